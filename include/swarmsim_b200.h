@@ -1,0 +1,232 @@
+/* swarmsim_b200.h — C-ABI of the B200 batched environment step.
+ *
+ * The reference (swarmsim 0.1.0, pure Python + numpy) has no FFI; its hot
+ * path is the Python call chain
+ *     Env.step            /root/reference/pkg/src/swarmsim/env.py:209-235
+ *       decode_action     env.py:71-145
+ *       world_step        dynamics.py:123-184   (+ closest_points geometry.py:120,
+ *                                                collision_force dynamics.py:36,
+ *                                                integrate dynamics.py:69)
+ *       Scenario.post_step / reward / done / observation   env.py:227-233
+ *     Env.reset           env.py:189-198 -> Scenario.reset_world_at
+ *     lidar_scan          sensors.py:138-146
+ * Every entry point below replaces one of those seams with a stream-ordered
+ * launch.  All buffer pointers are DEVICE memory owned by the caller (the
+ * Python host side allocates them as torch tensors); the library borrows
+ * them for the duration of the call and never allocates inside a step.
+ * Only SsWorld (the static scene descriptor, the analog of the pair cache at
+ * core.py:247-251) is owned by the library.
+ *
+ * Return value: 0 on success, a negative SsStatus otherwise; the message is
+ * available from ss_last_error() (thread-local).
+ */
+#ifndef SWARMSIM_B200_H
+#define SWARMSIM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SS_ABI_VERSION 1
+#define SS_RNG_WORDS 12          /* counter[4] key[2] buffer[4] buffer_pos spare */
+#define SS_MAX_ENTITIES 1024
+#define SS_MAX_AGENTS 256
+#define SS_MAX_RESET_OPS 1024
+
+typedef enum SsStatus {
+  SS_OK = 0,
+  SS_ERR_CONTRACT = -1,        /* -> ContractViolation   (errors.py:8)  */
+  SS_ERR_SHAPE_PAIR = -2,      /* -> UnsupportedShapePair (errors.py:12) */
+  SS_ERR_SCENARIO = -3,        /* -> UnknownScenario      (errors.py:16) */
+  SS_ERR_CUDA = -4,            /* CUDA launch / runtime failure          */
+  SS_ERR_UNSUPPORTED = -5      /* size not instantiated for a fused kernel */
+} SsStatus;
+
+typedef enum SsShape { SS_SPHERE = 0, SS_BOX = 1, SS_LINE = 2 } SsShape;
+
+typedef enum SsScenario {
+  SS_SCN_PHYSICS_ONLY = 0,     /* world_step only; reward/obs by Python hooks */
+  SS_SCN_SIMPLE_SPREAD = 1,    /* scenarios/simple_spread.py */
+  SS_SCN_TRANSPORT = 2,        /* scenarios/transport.py     */
+  SS_SCN_FLOCKING = 3,         /* scenarios/flocking.py (+ optional Lidar obs) */
+  SS_SCN_DISPERSION = 4,       /* scenarios/dispersion.py    */
+  SS_SCN_DISCOVERY = 5         /* scenarios/discovery.py     */
+} SsScenario;
+
+/* Step phases (bit flags of SsStepIO.mode). A full Env.step is SS_MODE_STEP. */
+enum {
+  SS_DO_PHYSICS = 1,   /* decode + world_step                  env.py:218-226 */
+  SS_DO_POST = 2,      /* scenario.post_step                   env.py:227     */
+  SS_DO_COUNT = 4,     /* step_count += 1                      env.py:228     */
+  SS_DO_REWARD = 8,    /* rewards                              env.py:229-231 */
+  SS_DO_DONE = 16,     /* dones = done | step_count>=max_steps  env.py:232     */
+  SS_DO_OBS = 32,      /* observations                         env.py:233     */
+  SS_MODE_STEP = 63
+};
+
+/* Per-entity static descriptor (core.py:120-198, shapes.py:15-73). Float
+ * fields are pre-rounded on the host exactly as numpy rounds them. */
+typedef struct SsEntityDesc {
+  int32_t shape;          /* SsShape */
+  int32_t movable, rotatable, collidable;
+  int32_t is_agent;
+  int32_t slot;           /* movable: row of dyn[]; else row of stat[]        */
+  double dim0, dim1;      /* sphere radius | box length,width | line length (python floats) */
+  float inv_m_dt;         /* f32(f32(1/mass) * f32(dt))     dynamics.py:78   */
+  float inv_i_dt;         /* f32(f32(1/moi)  * f32(dt))     dynamics.py:84   */
+  float max_speed;        /* f32(max_speed); <= 0 means None                  */
+  float grav_x, grav_y;   /* f32(g) * f32(mass)             dynamics.py:154  */
+  float u_range;          /* agents: clip bound            env.py:97         */
+  float u_mult;           /* agents: f32(u_multiplier)                        */
+} SsEntityDesc;
+
+/* One collidable pair (i < j) of the static pair list (dynamics.py:89-100). */
+typedef struct SsPairDesc {
+  int32_t i, j;
+  float d_min;            /* f32(min_contact_distance)      shapes.py:65     */
+  float sign;             /* +1 if (i+j) even else -1       dynamics.py:169  */
+} SsPairDesc;
+
+/* One reset action in scenario call order (common.py:11-34). */
+typedef struct SsResetOp {
+  int32_t entity;         /* entity index */
+  int32_t kind;           /* 0 = scatter (2 draws), 1 = place */
+  double lo_x, lo_y;      /* scatter: lower corner | place: x, y */
+  double range_x, range_y;/* scatter: hi - lo (float64, as numpy computes)    */
+} SsResetOp;
+
+typedef struct SsWorldDesc {
+  int32_t abi_version;    /* SS_ABI_VERSION */
+  int32_t scenario;       /* SsScenario */
+  int32_t n_entities;     /* agents first (core.py:237-242) */
+  int32_t n_agents;
+  int32_t n_dyn, n_stat;  /* rows of the dyn / stat state buffers */
+  int32_t obs_dim;        /* per-agent observation width */
+  int32_t n_flag_words;   /* uint32 rows of SsBuffers.flags */
+  int64_t batch;          /* envs held by this process (shard) */
+  int64_t env_offset;     /* global index of local env 0 */
+  int64_t global_batch;   /* envs across all shards (RNG stream layout) */
+  int64_t max_steps;
+  float dt;               /* f32(dt) */
+  float keep;             /* f32(1 - damping) */
+  float contact_ck;       /* f32(contact_force * contact_margin) */
+  float contact_k;        /* f32(contact_margin) */
+  int32_t has_gravity;
+  int32_t n_pairs;
+  const SsEntityDesc* entities;
+  const SsPairDesc* pairs;
+  int32_t n_reset_ops;
+  const SsResetOp* reset_ops;
+  float sc[16];           /* scenario float32 constants */
+  double sd[8];           /* scenario float64 constants */
+  int32_t si[8];          /* scenario int constants */
+  /* optional Lidar appended to each agent's observation (flocking config) */
+  int32_t lidar_rays;     /* 0 = none */
+  int32_t lidar_attach_rotation;
+  double lidar_max_range;
+  double lidar_start, lidar_span;
+  const double* lidar_dirs;   /* HOST [lidar_rays][2]: numpy cos/sin of the rot=0 angles */
+} SsWorldDesc;
+
+/* Device state, all row-major [row][B][...], env index contiguous. */
+typedef struct SsBuffers {
+  float* dyn;             /* [n_dyn][B][4]  px py vx vy of movable entities */
+  float* stat;            /* [n_stat][B][2] position of non-movable entities */
+  float* stat_vel;        /* [n_stat][B][2] velocity of non-movable entities */
+  float* rot;             /* [n_entities][B][2] rot, ang_vel */
+  int64_t* step_count;    /* [B] */
+  uint32_t* flags;        /* [n_flag_words][B] scenario bit flags */
+  float* aux;             /* [B] scenario scalar (dispersion fresh_bites) */
+  uint64_t* rng;          /* [2][SS_RNG_WORDS] double-buffered Philox state */
+  int32_t rng_cur;        /* which half of rng[] is current (input) */
+} SsBuffers;
+
+typedef struct SsStepIO {
+  const float* const* actions; /* HOST array of n_agents device pointers, each [B][2] f32 */
+  float* obs;             /* obs of agent a, env e at obs[a*obs_agent_stride + e*obs_dim] */
+  int64_t obs_agent_stride;
+  float* rew;             /* [n_agents][B] */
+  uint8_t* done;          /* [B] */
+  int32_t mode;           /* SS_DO_* flags */
+  const int32_t* guard;   /* optional device flag: if *guard != 0 the launch is a no-op */
+  int32_t raw_forces;     /* nonzero: actions are final forces (discrete / noisy /
+                             scripted agents decoded by the host); skip decode_action */
+} SsStepIO;
+
+typedef struct SsLidarDesc {
+  int32_t n_rays;
+  double max_range;       /* compared/returned as in sensors.py:135 */
+  double start_angle, span;  /* ray m: start + m*span/n_rays (+ rot) */
+  int32_t attach_rotation;
+  const double* dir_table;   /* optional device [n_rays][2] cos/sin for rot == 0 */
+} SsLidarDesc;
+
+int ss_abi_version(void);
+const char* ss_last_error(void);
+
+/* Build / free the static scene descriptor (pair list, constants, reset
+ * program) for one World.  Replaces the Python pair cache core.py:247-251. */
+int ss_world_create(const SsWorldDesc* desc, void** out_world);
+int ss_world_destroy(void* world);
+
+/* One fused Env.step for every env (env.py:209-235).  For scenario
+ * SS_SCN_PHYSICS_ONLY only SS_DO_PHYSICS|SS_DO_COUNT apply (world_step,
+ * dynamics.py:123-184). */
+int ss_env_step(void* world, const SsBuffers* buf, const SsStepIO* io, void* stream);
+
+/* Env.reset (env.py:189-198) -> Scenario.reset_world_at.  mask == NULL
+ * resets every env with the reference's whole-batch draw order (x block then
+ * y block per scatter, batching.py:212-213); otherwise mask[B] (uint8) resets
+ * the selected envs exactly as sequential reset(env_index=i) calls in
+ * ascending i.  `mask_base` (device, may be NULL) is the number of selected
+ * envs on lower shards and `mask_total` (device, may be NULL) the selected
+ * count over all shards; both NULL means unsharded.  Advances buf->rng into
+ * the other half; the caller flips rng_cur afterwards. */
+int ss_reset(void* world, const SsBuffers* buf, const uint8_t* mask,
+             const int64_t* mask_base, const int64_t* mask_total, void* stream);
+
+/* Count of selected envs in mask[B] into *count_out (device int64). */
+int ss_mask_count(void* world, const uint8_t* mask, int64_t* count_out, void* stream);
+
+/* NaN scan of the actions (env.py:85, dynamics.py:112): sets *flag_out
+ * (device int32) to nonzero when any value is NaN.  Does not clear it. */
+int ss_check_actions(void* world, const float* const* actions, int32_t* flag_out, void* stream);
+
+/* lidar_scan (sensors.py:138-146) for one agent: out[B][n_rays] f32. */
+int ss_lidar(void* world, const SsBuffers* buf, int32_t agent, const SsLidarDesc* lidar,
+             float* out, void* stream);
+
+/* cast_ray (sensors.py:113-135): out[e] = nearest hit from (ox[e], oy[e])
+ * along angle[e] (float64), skipping entity `exclude` (-1: none). */
+int ss_cast_ray(void* world, const SsBuffers* buf, int32_t exclude, const float* ox,
+                const float* oy, const double* angle, double max_range, float* out, void* stream);
+
+/* Function-level seams used by the reference's unit tests. All arrays [n]. */
+/* collision_force (dynamics.py:36-66): force on i and the active mask. */
+int ss_collision_force(const float* pix, const float* piy, const float* pjx, const float* pjy,
+                       float d_min, float sign, float contact_ck, float contact_k,
+                       float* fx, float* fy, uint8_t* active, int64_t n, void* stream);
+/* closest_points (geometry.py:120-163) between two posed shapes.  Shape
+ * dimensions are the Python floats of shapes.py.  *d_status (device int32)
+ * is set nonzero on an unsupported pair. */
+int ss_closest_points(const float* pos_i /*[n][2]*/, const float* rot_i, int32_t shape_i,
+                      double dim_i0, double dim_i1,
+                      const float* pos_j /*[n][2]*/, const float* rot_j, int32_t shape_j,
+                      double dim_j0, double dim_j1,
+                      float* out_i /*[n][2]*/, float* out_j /*[n][2]*/, int64_t n,
+                      int32_t* d_status, void* stream);
+
+/* Module-level world_step(world, actions) (dynamics.py:123-184) for any
+ * world: forces[a] is agent a's force [B][2] (device); decode_mask bit a
+ * (4 x uint64, NULL = all) applies decode_action's clip*u_multiplier to it
+ * (Env.step path) instead of using it as-is (AgentAction / action_script
+ * path).  count != 0 also increments step_count.  *d_status as above. */
+int ss_world_step(void* world, const SsBuffers* buf, const float* const* forces,
+                  const uint64_t* decode_mask, int32_t count, int32_t* d_status, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SWARMSIM_B200_H */

@@ -1,0 +1,239 @@
+// ss_capi.cu — the extern "C" boundary (include/swarmsim_b200.h).
+#include <cstdio>
+#include <new>
+
+#include "ss_geometry.cuh"
+
+namespace ss {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return SS_OK;
+  set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return SS_ERR_CUDA;
+}
+
+int launch_small(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_t st);
+int launch_large(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_t st);
+int launch_generic(World& w, const SsBuffers* buf, const SsStepIO* io, const uint64_t* decode_mask,
+                   int* d_status, cudaStream_t st);
+int launch_reset(World& w, const SsBuffers* buf, const uint8_t* mask, const int64_t* mask_base,
+                 const int64_t* mask_total, cudaStream_t st);
+int launch_mask_count(World& w, const uint8_t* mask, int64_t* count_out, cudaStream_t st);
+int launch_check_actions(int n_agents, int64_t B, const float* const* actions, int* flag,
+                         cudaStream_t st);
+int launch_collision_force(const float* pix, const float* piy, const float* pjx, const float* pjy,
+                           float dmin, float sign, float ck, float k, float* fx, float* fy,
+                           uint8_t* active, int64_t n, cudaStream_t st);
+int launch_closest_points(const float* pos_i, const float* rot_i, ShapeK si, const float* pos_j,
+                          const float* rot_j, ShapeK sj, float* out_i, float* out_j, int64_t n,
+                          int* status, cudaStream_t st);
+int launch_lidar(World& w, const SsBuffers* buf, int agent, const SsLidarDesc* lidar, float* out,
+                 cudaStream_t st);
+int launch_cast_ray(World& w, const SsBuffers* buf, int exclude, const float* ox, const float* oy,
+                    const double* angle, double max_range, float* out, cudaStream_t st);
+
+template <class T>
+static int upload(const std::vector<T>& v, T** dst) {
+  *dst = nullptr;
+  if (v.empty()) return SS_OK;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(dst), v.size() * sizeof(T));
+  if (e != cudaSuccess) return cuda_status(e, "cudaMalloc (world tables)");
+  e = cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+  return cuda_status(e, "cudaMemcpy (world tables)");
+}
+
+static void free_world(World* w) {
+  if (!w) return;
+  cudaFree(w->d_ents);
+  cudaFree(w->d_pairs);
+  cudaFree(w->d_reset_ops);
+  cudaFree(w->d_lidar_dirs);
+  cudaFree(w->d_scan);
+  delete w;
+}
+
+static int validate_desc(const SsWorldDesc* d) {
+  if (!d) { set_error("null world descriptor"); return SS_ERR_CONTRACT; }
+  if (d->abi_version != SS_ABI_VERSION) {
+    set_error("ABI version mismatch: library " + std::to_string(SS_ABI_VERSION) + ", caller " +
+              std::to_string(d->abi_version));
+    return SS_ERR_CONTRACT;
+  }
+  if (d->batch < 1) { set_error("batch_size must be >= 1"); return SS_ERR_CONTRACT; }
+  if (d->n_entities < 0 || d->n_entities > SS_MAX_ENTITIES) { set_error("bad entity count"); return SS_ERR_CONTRACT; }
+  if (d->n_agents < 0 || d->n_agents > d->n_entities || d->n_agents > SS_MAX_AGENTS) {
+    set_error("bad agent count"); return SS_ERR_CONTRACT;
+  }
+  if (d->global_batch < d->batch || d->env_offset < 0 || d->env_offset + d->batch > d->global_batch) {
+    set_error("shard [env_offset, env_offset+batch) outside global_batch"); return SS_ERR_CONTRACT;
+  }
+  if (d->scenario < SS_SCN_PHYSICS_ONLY || d->scenario > SS_SCN_DISCOVERY) {
+    set_error("unknown scenario id " + std::to_string(d->scenario)); return SS_ERR_SCENARIO;
+  }
+  if (d->n_reset_ops < 0 || d->n_reset_ops > SS_MAX_RESET_OPS) { set_error("bad reset program"); return SS_ERR_CONTRACT; }
+  for (int k = 0; k < d->n_entities; ++k) {
+    const SsEntityDesc& e = d->entities[k];
+    if (e.shape < SS_SPHERE || e.shape > SS_LINE) {
+      set_error("entity " + std::to_string(k) + " has an unsupported shape");
+      return SS_ERR_SHAPE_PAIR;
+    }
+    const int rows = e.movable ? d->n_dyn : d->n_stat;
+    if (e.slot < 0 || e.slot >= rows) { set_error("entity slot out of range"); return SS_ERR_CONTRACT; }
+  }
+  for (int p = 0; p < d->n_pairs; ++p) {
+    const SsPairDesc& q = d->pairs[p];
+    if (q.i < 0 || q.j <= q.i || q.j >= d->n_entities) { set_error("bad pair list"); return SS_ERR_CONTRACT; }
+  }
+  for (int j = 0; j < d->n_reset_ops; ++j) {
+    const SsResetOp& o = d->reset_ops[j];
+    if (o.entity < 0 || o.entity >= d->n_entities || (o.kind != 0 && o.kind != 1)) {
+      set_error("bad reset op"); return SS_ERR_CONTRACT;
+    }
+  }
+  return SS_OK;
+}
+
+}  // namespace ss
+
+using namespace ss;
+
+extern "C" {
+
+int ss_abi_version(void) { return SS_ABI_VERSION; }
+
+const char* ss_last_error(void) { return g_last_error.c_str(); }
+
+int ss_world_create(const SsWorldDesc* desc, void** out_world) {
+  if (!out_world) { set_error("null out pointer"); return SS_ERR_CONTRACT; }
+  *out_world = nullptr;
+  int rc = validate_desc(desc);
+  if (rc) return rc;
+  World* w = new (std::nothrow) World();
+  if (!w) { set_error("out of host memory"); return SS_ERR_CUDA; }
+  w->d = *desc;
+  w->ents.assign(desc->entities, desc->entities + desc->n_entities);
+  w->pairs.assign(desc->pairs, desc->pairs + desc->n_pairs);
+  w->reset_ops.assign(desc->reset_ops, desc->reset_ops + desc->n_reset_ops);
+  w->n_scatter = 0;
+  for (const auto& o : w->reset_ops) w->n_scatter += (o.kind == 0);
+  if ((rc = upload(w->ents, &w->d_ents)) || (rc = upload(w->pairs, &w->d_pairs)) ||
+      (rc = upload(w->reset_ops, &w->d_reset_ops))) {
+    free_world(w);
+    return rc;
+  }
+  if (desc->lidar_rays > 0) {
+    std::vector<double> dirs(desc->lidar_dirs, desc->lidar_dirs + 2 * desc->lidar_rays);
+    if ((rc = upload(dirs, &w->d_lidar_dirs))) { free_world(w); return rc; }
+  }
+  w->scan_cap = (desc->batch + 255) / 256 + 2;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&w->d_scan), w->scan_cap * sizeof(int64_t));
+  if (e != cudaSuccess) { free_world(w); return cuda_status(e, "cudaMalloc (scan scratch)"); }
+  // the struct copy still points at caller memory; never read those again
+  w->d.entities = nullptr;
+  w->d.pairs = nullptr;
+  w->d.reset_ops = nullptr;
+  w->d.lidar_dirs = nullptr;
+  *out_world = w;
+  return SS_OK;
+}
+
+int ss_world_destroy(void* world) {
+  free_world(static_cast<World*>(world));
+  return SS_OK;
+}
+
+int ss_env_step(void* world, const SsBuffers* buf, const SsStepIO* io, void* stream) {
+  World* w = static_cast<World*>(world);
+  if (!w || !buf || !io) { set_error("null argument"); return SS_ERR_CONTRACT; }
+  if ((io->mode & SS_DO_PHYSICS) && w->d.n_agents > 0 && !io->actions) {
+    set_error("actions required for a physics step"); return SS_ERR_CONTRACT;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (w->d.scenario) {
+    case SS_SCN_SIMPLE_SPREAD:
+    case SS_SCN_TRANSPORT:
+    case SS_SCN_FLOCKING:
+      return launch_small(*w, buf, io, st);
+    case SS_SCN_DISPERSION:
+    case SS_SCN_DISCOVERY:
+      return launch_large(*w, buf, io, st);
+    default:
+      return launch_generic(*w, buf, io, nullptr, nullptr, st);
+  }
+}
+
+int ss_world_step(void* world, const SsBuffers* buf, const float* const* forces,
+                  const uint64_t* decode_mask, int32_t count, int32_t* d_status, void* stream) {
+  World* w = static_cast<World*>(world);
+  if (!w || !buf) { set_error("null argument"); return SS_ERR_CONTRACT; }
+  SsStepIO io;
+  memset(&io, 0, sizeof(io));
+  io.actions = forces;
+  io.mode = SS_DO_PHYSICS | (count ? SS_DO_COUNT : 0);
+  return launch_generic(*w, buf, &io, decode_mask, d_status, static_cast<cudaStream_t>(stream));
+}
+
+int ss_reset(void* world, const SsBuffers* buf, const uint8_t* mask, const int64_t* mask_base,
+             const int64_t* mask_total, void* stream) {
+  World* w = static_cast<World*>(world);
+  if (!w || !buf) { set_error("null argument"); return SS_ERR_CONTRACT; }
+  return launch_reset(*w, buf, mask, mask_base, mask_total, static_cast<cudaStream_t>(stream));
+}
+
+int ss_mask_count(void* world, const uint8_t* mask, int64_t* count_out, void* stream) {
+  World* w = static_cast<World*>(world);
+  if (!w || !mask || !count_out) { set_error("null argument"); return SS_ERR_CONTRACT; }
+  return launch_mask_count(*w, mask, count_out, static_cast<cudaStream_t>(stream));
+}
+
+int ss_check_actions(void* world, const float* const* actions, int32_t* flag_out, void* stream) {
+  World* w = static_cast<World*>(world);
+  if (!w || !flag_out) { set_error("null argument"); return SS_ERR_CONTRACT; }
+  return launch_check_actions(w->d.n_agents, w->d.batch, actions, flag_out,
+                              static_cast<cudaStream_t>(stream));
+}
+
+int ss_lidar(void* world, const SsBuffers* buf, int32_t agent, const SsLidarDesc* lidar,
+             float* out, void* stream) {
+  World* w = static_cast<World*>(world);
+  if (!w || !buf || !lidar || !out) { set_error("null argument"); return SS_ERR_CONTRACT; }
+  if (agent < 0 || agent >= w->d.n_entities) { set_error("emitter index out of range"); return SS_ERR_CONTRACT; }
+  if (lidar->n_rays < 1) { set_error("n_rays must be >= 1"); return SS_ERR_CONTRACT; }
+  return launch_lidar(*w, buf, agent, lidar, out, static_cast<cudaStream_t>(stream));
+}
+
+int ss_cast_ray(void* world, const SsBuffers* buf, int32_t exclude, const float* ox,
+                const float* oy, const double* angle, double max_range, float* out, void* stream) {
+  World* w = static_cast<World*>(world);
+  if (!w || !buf || !ox || !oy || !angle || !out) { set_error("null argument"); return SS_ERR_CONTRACT; }
+  return launch_cast_ray(*w, buf, exclude, ox, oy, angle, max_range, out,
+                         static_cast<cudaStream_t>(stream));
+}
+
+int ss_collision_force(const float* pix, const float* piy, const float* pjx, const float* pjy,
+                       float d_min, float sign, float contact_ck, float contact_k, float* fx,
+                       float* fy, uint8_t* active, int64_t n, void* stream) {
+  return launch_collision_force(pix, piy, pjx, pjy, d_min, sign, contact_ck, contact_k, fx, fy,
+                                active, n, static_cast<cudaStream_t>(stream));
+}
+
+int ss_closest_points(const float* pos_i, const float* rot_i, int32_t shape_i, double dim_i0,
+                      double dim_i1, const float* pos_j, const float* rot_j, int32_t shape_j,
+                      double dim_j0, double dim_j1, float* out_i, float* out_j, int64_t n,
+                      int32_t* d_status, void* stream) {
+  ShapeK si, sj;
+  si.kind = shape_i; si.d0 = dim_i0; si.d1 = dim_i1;
+  sj.kind = shape_j; sj.d0 = dim_j0; sj.d1 = dim_j1;
+  if (shape_i < SS_SPHERE || shape_i > SS_LINE || shape_j < SS_SPHERE || shape_j > SS_LINE) {
+    set_error("unsupported shape pair");
+    return SS_ERR_SHAPE_PAIR;
+  }
+  return launch_closest_points(pos_i, rot_i, si, pos_j, rot_j, sj, out_i, out_j, n, d_status,
+                               static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

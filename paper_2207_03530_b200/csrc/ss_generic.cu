@@ -1,0 +1,221 @@
+// ss_generic.cu — world_step for arbitrary worlds (dynamics.py:123-184) plus
+// the function-level seams (collision_force, closest_points) and the action
+// NaN scan.  Used by user-defined scenarios (reward/obs in Python hooks), by
+// the catalog scenarios without a fused kernel, and by the module-level
+// world_step() API.  One thread per env; the per-entity force/torque
+// accumulators of a warp's 32 envs live in shared memory ([E][32] each) so
+// any entity count and any pair list run through the same code.
+#include "ss_geometry.cuh"
+
+namespace ss {
+
+constexpr int kGenericMaxAgents = 256;
+
+struct GenericArgs {
+  DevState s;
+  PhysK ph;
+  const SsEntityDesc* ents;
+  const SsPairDesc* pairs;
+  int E, A, P;
+  const float2* act[kGenericMaxAgents];
+  uint64_t decode_mask[kGenericMaxAgents / 64];  // bit i: decode_action applies
+  int mode;
+  const int* guard;
+  int* status;   // set to 1 when an unsupported shape pair is met
+};
+
+SS_DEV V2 load_pos(const DevState& s, const SsEntityDesc& d, int64_t e) {
+  if (d.movable) { const float4 q = s.dyn[d.slot * s.B + e]; return v2(q.x, q.y); }
+  const float2 q = s.stat[d.slot * s.B + e];
+  return v2(q.x, q.y);
+}
+
+__global__ void __launch_bounds__(32) k_generic_physics(const GenericArgs a) {
+  extern __shared__ float sm[];
+  if (a.guard && *a.guard) return;
+  const int lane = threadIdx.x;
+  const int64_t B = a.s.B;
+  const int64_t e = (int64_t)blockIdx.x * 32 + lane;
+  if (e >= B) return;
+  if (!(a.mode & SS_DO_PHYSICS)) {
+    if (a.mode & SS_DO_COUNT) a.s.step_count[e] += 1;
+    return;
+  }
+  float* FX = sm;
+  float* FY = sm + a.E * 32;
+  float* TQ = sm + 2 * a.E * 32;
+  for (int k = 0; k < a.E; ++k) { FX[k * 32 + lane] = 0.0f; FY[k * 32 + lane] = 0.0f; TQ[k * 32 + lane] = 0.0f; }
+  // action forces (dynamics.py:151-152); decode_action (env.py:97) when flagged
+  for (int i = 0; i < a.A; ++i) {
+    if (a.act[i] == nullptr) continue;
+    const float2 u = a.act[i][e];
+    float fx = u.x, fy = u.y;
+    if ((a.decode_mask[i >> 6] >> (i & 63)) & 1ull) {
+      const SsEntityDesc& d = a.ents[i];
+      fx = fmul(clip_sym(u.x, d.u_range), d.u_mult);
+      fy = fmul(clip_sym(u.y, d.u_range), d.u_mult);
+    }
+    FX[i * 32 + lane] = fadd(0.0f, fx);
+    FY[i * 32 + lane] = fadd(0.0f, fy);
+  }
+  if (a.ph.has_gravity) {  // dynamics.py:154-161
+    for (int k = 0; k < a.E; ++k) {
+      const SsEntityDesc& d = a.ents[k];
+      if (!d.movable) continue;
+      FX[k * 32 + lane] = fadd(FX[k * 32 + lane], d.grav_x);
+      FY[k * 32 + lane] = fadd(FY[k * 32 + lane], d.grav_y);
+    }
+  }
+  // pair contacts in pair-list order (dynamics.py:163-180)
+  for (int p = 0; p < a.P; ++p) {
+    const SsPairDesc pr = a.pairs[p];
+    const SsEntityDesc& di = a.ents[pr.i];
+    const SsEntityDesc& dj = a.ents[pr.j];
+    const V2 pi = load_pos(a.s, di, e), pj = load_pos(a.s, dj, e);
+    const float ri = a.s.rot[pr.i * B + e].x, rj = a.s.rot[pr.j * B + e].x;
+    ShapeK si, sj;
+    si.kind = di.shape; si.d0 = di.dim0; si.d1 = di.dim1;
+    sj.kind = dj.shape; sj.d0 = dj.dim0; sj.d1 = dj.dim1;
+    V2 oi, oj;
+    if (!closest_points(pi, ri, si, pj, rj, sj, oi, oj)) { *a.status = 1; return; }
+    float fx, fy;
+    if (!contact_force(oi.x, oi.y, oj.x, oj.y, pr.d_min, pr.sign, a.ph.ck, a.ph.k, fx, fy)) continue;
+    FX[pr.i * 32 + lane] = fadd(FX[pr.i * 32 + lane], fx);
+    FY[pr.i * 32 + lane] = fadd(FY[pr.i * 32 + lane], fy);
+    FX[pr.j * 32 + lane] = fsub(FX[pr.j * 32 + lane], fx);
+    FY[pr.j * 32 + lane] = fsub(FY[pr.j * 32 + lane], fy);
+    if (di.rotatable) {
+      const V2 r = vsub(oi, pi);
+      TQ[pr.i * 32 + lane] = fadd(TQ[pr.i * 32 + lane], fsub(fmul(r.x, fy), fmul(r.y, fx)));
+    }
+    if (dj.rotatable) {
+      const V2 r = vsub(oj, pj);
+      TQ[pr.j * 32 + lane] = fsub(TQ[pr.j * 32 + lane], fsub(fmul(r.x, fy), fmul(r.y, fx)));
+    }
+  }
+  // integrate (dynamics.py:182-184)
+  for (int k = 0; k < a.E; ++k) {
+    const SsEntityDesc& d = a.ents[k];
+    if (d.movable) {
+      float4 q = a.s.dyn[d.slot * B + e];
+      integrate_lin(q.x, q.y, q.z, q.w, FX[k * 32 + lane], FY[k * 32 + lane], a.ph.keep,
+                    d.inv_m_dt, a.ph.dt, d.max_speed);
+      a.s.dyn[d.slot * B + e] = q;
+    }
+    if (d.rotatable) {
+      float2 r = a.s.rot[k * B + e];
+      integrate_ang(r.x, r.y, TQ[k * 32 + lane], a.ph.keep, d.inv_i_dt, a.ph.dt);
+      a.s.rot[k * B + e] = r;
+    }
+  }
+  if (a.mode & SS_DO_COUNT) a.s.step_count[e] += 1;
+}
+
+int launch_generic(World& w, const SsBuffers* buf, const SsStepIO* io, const uint64_t* decode_mask,
+                   int* d_status, cudaStream_t st) {
+  GenericArgs a;
+  memset(&a, 0, sizeof(a));
+  a.s = make_state(w, buf);
+  a.ph = make_phys(w);
+  a.ents = w.d_ents;
+  a.pairs = w.d_pairs;
+  a.E = w.d.n_entities;
+  a.A = w.d.n_agents;
+  a.P = w.d.n_pairs;
+  if (a.A > kGenericMaxAgents) { set_error("too many agents for world_step"); return SS_ERR_UNSUPPORTED; }
+  if (io->mode & SS_DO_PHYSICS) {
+    for (int i = 0; i < a.A; ++i) a.act[i] = reinterpret_cast<const float2*>(io->actions[i]);
+    for (int i = 0; i < kGenericMaxAgents / 64; ++i) a.decode_mask[i] = decode_mask ? decode_mask[i] : ~0ull;
+  }
+  a.mode = io->mode;
+  a.guard = io->guard;
+  a.status = d_status;
+  if (!(io->mode & (SS_DO_PHYSICS | SS_DO_COUNT))) return SS_OK;
+  const size_t shmem = (size_t)3 * a.E * 32 * sizeof(float);
+  if (shmem > 200 * 1024) { set_error("world too large for the generic step kernel"); return SS_ERR_UNSUPPORTED; }
+  if (shmem > 48 * 1024) {
+    cudaFuncSetAttribute(k_generic_physics, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
+  }
+  const unsigned grid = (unsigned)((w.d.batch + 31) / 32);
+  k_generic_physics<<<grid, 32, shmem, st>>>(a);
+  return cuda_status(cudaGetLastError(), "generic world_step launch");
+}
+
+// ---- function-level kernels -------------------------------------------------
+__global__ void k_collision_force(const float* pix, const float* piy, const float* pjx,
+                                  const float* pjy, float dmin, float sign, float ck, float k,
+                                  float* fx, float* fy, uint8_t* active, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float x, y;
+  active[i] = contact_force(pix[i], piy[i], pjx[i], pjy[i], dmin, sign, ck, k, x, y) ? 1 : 0;
+  fx[i] = x;
+  fy[i] = y;
+}
+
+__global__ void k_closest_points(const float2* pos_i, const float* rot_i, ShapeK si,
+                                 const float2* pos_j, const float* rot_j, ShapeK sj,
+                                 float2* out_i, float2* out_j, int64_t n, int* status) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  V2 oi, oj;
+  const float2 a = pos_i[i], b = pos_j[i];
+  if (!closest_points(v2(a.x, a.y), rot_i[i], si, v2(b.x, b.y), rot_j[i], sj, oi, oj)) {
+    *status = 1;
+    return;
+  }
+  out_i[i] = make_float2(oi.x, oi.y);
+  out_j[i] = make_float2(oj.x, oj.y);
+}
+
+struct CheckArgs {
+  const float* act[kGenericMaxAgents];
+  int64_t n;   // floats per agent
+  int* flag;
+};
+
+__global__ void k_check_actions(const CheckArgs a) {
+  const float* p = a.act[blockIdx.y];
+  bool bad = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    bad |= isnan(p[i]);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(a.flag, 1);
+}
+
+int launch_check_actions(int n_agents, int64_t B, const float* const* actions, int* flag,
+                         cudaStream_t st) {
+  if (n_agents > kGenericMaxAgents) { set_error("too many agents"); return SS_ERR_UNSUPPORTED; }
+  if (n_agents == 0) return SS_OK;
+  CheckArgs a;
+  memset(&a, 0, sizeof(a));
+  for (int i = 0; i < n_agents; ++i) a.act[i] = actions[i];
+  a.n = 2 * B;
+  a.flag = flag;
+  const int64_t want = (a.n + 255) / 256;
+  const unsigned gx = (unsigned)(want < 1184 ? want : 1184);
+  k_check_actions<<<dim3(gx, n_agents), 256, 0, st>>>(a);
+  return cuda_status(cudaGetLastError(), "action check launch");
+}
+
+int launch_collision_force(const float* pix, const float* piy, const float* pjx, const float* pjy,
+                           float dmin, float sign, float ck, float k, float* fx, float* fy,
+                           uint8_t* active, int64_t n, cudaStream_t st) {
+  if (n <= 0) return SS_OK;
+  k_collision_force<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pix, piy, pjx, pjy, dmin, sign,
+                                                                 ck, k, fx, fy, active, n);
+  return cuda_status(cudaGetLastError(), "collision_force launch");
+}
+
+int launch_closest_points(const float* pos_i, const float* rot_i, ShapeK si, const float* pos_j,
+                          const float* rot_j, ShapeK sj, float* out_i, float* out_j, int64_t n,
+                          int* status, cudaStream_t st) {
+  if (n <= 0) return SS_OK;
+  k_closest_points<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+      reinterpret_cast<const float2*>(pos_i), rot_i, si, reinterpret_cast<const float2*>(pos_j),
+      rot_j, sj, reinterpret_cast<float2*>(out_i), reinterpret_cast<float2*>(out_j), n, status);
+  return cuda_status(cudaGetLastError(), "closest_points launch");
+}
+
+}  // namespace ss

@@ -1,0 +1,525 @@
+// ss_small.cu — fused Env.step for the small built-in scenarios
+// (simple_spread, transport, flocking): one thread per environment, the whole
+// entity state of an env lives in registers for the duration of the step.
+//
+// One launch does, per env (env.py:209-235 order):
+//   decode (env.py:97) -> forces: action, gravity, pair contacts in the
+//   reference's lexicographic pair order (dynamics.py:151-180) -> integrate
+//   (dynamics.py:182-184) -> post_step -> step_count += 1 -> rewards ->
+//   done | horizon -> observations.
+// HBM traffic: every state row read once and written once (float4 SoA rows,
+// env index contiguous, so each warp access is a contiguous 512 B), actions
+// read once, obs/reward/done written once (obs staged per warp in shared
+// memory and streamed out with 16-byte stores).
+#include "ss_internal.cuh"
+
+namespace ss {
+
+constexpr int kSmallMaxAgents = 8;
+constexpr int kFlockMaxRocks = 6;
+constexpr int kSmallThreads = 128;
+
+struct SmallArgs {
+  DevState s;
+  PhysK ph;
+  const SsEntityDesc* ents;
+  const SsPairDesc* pairs;
+  const float2* act[kSmallMaxAgents];
+  float* obs;
+  int64_t obs_stride;   // floats between agent blocks
+  float* rew;
+  uint8_t* done;
+  int mode;
+  int raw_forces;
+  int obs_dim;
+  const int* guard;
+  float sc[16];
+  double sd[8];
+  int si[8];
+  // lidar (flocking extension)
+  int n_rays;
+  double lidar_range;
+  double ray_start, ray_span;
+  int attach_rot;
+  const double* ray_dir;  // [n_rays][2] cos/sin of the base angles (numpy values)
+};
+
+// Flush one agent's staged obs rows (warp-private smem) to global memory.
+SS_DEV void warp_flush(float* __restrict__ dst, int nvalid, int O, float* __restrict__ sbuf) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+  const int n = nvalid * O;
+  if ((reinterpret_cast<uintptr_t>(dst) & 15u) != 0) {
+    for (int i = lane; i < n; i += 32) __stcs(dst + i, sbuf[i]);
+    __syncwarp();
+    return;
+  }
+  const int n4 = n >> 2;
+  float4* d4 = reinterpret_cast<float4*>(dst);
+  const float4* s4 = reinterpret_cast<const float4*>(sbuf);
+  for (int i = lane; i < n4; i += 32) __stcs(d4 + i, s4[i]);
+  for (int i = (n4 << 2) + lane; i < n; i += 32) __stcs(dst + i, sbuf[i]);
+  __syncwarp();
+}
+
+// decode_action's continuous branch (env.py:96-98) unless the host already
+// produced final forces.
+SS_DEV float decode_axis(float raw, const SsEntityDesc& d, int raw_forces) {
+  return raw_forces ? raw : fmul(clip_sym(raw, d.u_range), d.u_mult);
+}
+
+// fp64 ray vs circle (sensors.py:43-54); inf on miss.
+SS_DEV double ray_circle(double ox, double oy, double dx, double dy, double cx, double cy,
+                         double r2) {
+  const double fx = dsub_rn(ox, cx), fy = dsub_rn(oy, cy);
+  const double b = dadd_rn(dmul_rn(fx, dx), dmul_rn(fy, dy));
+  const double c = dsub_rn(dadd_rn(dmul_rn(fx, fx), dmul_rn(fy, fy)), r2);
+  const double disc = dsub_rn(dmul_rn(b, b), c);
+  if (!(disc >= 0.0)) return __longlong_as_double(0x7ff0000000000000LL);
+  const double sq = sqrt(disc);
+  const double t1 = dsub_rn(-b, sq), t2 = dadd_rn(-b, sq);
+  if (t1 > 1e-9) return t1;
+  if (t2 > 1e-9) return t2;
+  return __longlong_as_double(0x7ff0000000000000LL);
+}
+
+// ---------------------------------------------------------------------------
+// simple_spread (scenarios/simple_spread.py): NA agents (dyn rows 0..NA-1),
+// NA markers (stat rows 0..NA-1). Pairs: agent-agent, lexicographic.
+// sc[0] = f32 touching threshold (r_a + r_b), sc[1] = f32(collision_penalty)
+// ---------------------------------------------------------------------------
+template <int NA>
+__global__ void __launch_bounds__(kSmallThreads) k_simple_spread(const SmallArgs a) {
+  extern __shared__ __align__(16) float smem[];
+  if (a.guard && *a.guard) return;
+  constexpr int O = 4 * NA + 2;
+  const int64_t B = a.s.B;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = e < B;
+  float px[NA], py[NA], vx[NA], vy[NA], mx[NA], my[NA];
+  if (valid) {
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      const float4 q = a.s.dyn[i * B + e];
+      px[i] = q.x; py[i] = q.y; vx[i] = q.z; vy[i] = q.w;
+      const float2 m = a.s.stat[i * B + e];
+      mx[i] = m.x; my[i] = m.y;
+    }
+  }
+  if (valid && (a.mode & SS_DO_PHYSICS)) {
+    float fx[NA], fy[NA];
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      const SsEntityDesc& d = a.ents[i];
+      const float2 u = a.act[i][e];
+      fx[i] = decode_axis(u.x, d, a.raw_forces);
+      fy[i] = decode_axis(u.y, d, a.raw_forces);
+      if (a.ph.has_gravity) { fx[i] = fadd(fx[i], d.grav_x); fy[i] = fadd(fy[i], d.grav_y); }
+    }
+    int p = 0;
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+#pragma unroll
+      for (int j = i + 1; j < NA; ++j, ++p) {
+        const SsPairDesc pr = a.pairs[p];
+        float cx, cy;
+        if (contact_force(px[i], py[i], px[j], py[j], pr.d_min, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
+          fx[i] = fadd(fx[i], cx); fy[i] = fadd(fy[i], cy);
+          fx[j] = fsub(fx[j], cx); fy[j] = fsub(fy[j], cy);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      const SsEntityDesc& d = a.ents[i];
+      integrate_lin(px[i], py[i], vx[i], vy[i], fx[i], fy[i], a.ph.keep, d.inv_m_dt, a.ph.dt,
+                    d.max_speed);
+      a.s.dyn[i * B + e] = make_float4(px[i], py[i], vx[i], vy[i]);
+    }
+  }
+  int64_t steps = 0;
+  if (valid && (a.mode & (SS_DO_COUNT | SS_DO_DONE))) {
+    steps = a.s.step_count[e];
+    if (a.mode & SS_DO_COUNT) { steps += 1; a.s.step_count[e] = steps; }
+  }
+  if (valid && (a.mode & SS_DO_REWARD)) {
+    const float thr = a.sc[0], pen = a.sc[1];
+    double cover = 0.0;   // np.zeros(B) float64 accumulator, simple_spread.py:41
+#pragma unroll
+    for (int m = 0; m < NA; ++m) {
+      float best = norm2(fsub(px[0], mx[m]), fsub(py[0], my[m]));
+#pragma unroll
+      for (int i = 1; i < NA; ++i) best = fminf(best, norm2(fsub(px[i], mx[m]), fsub(py[i], my[m])));
+      cover = dadd_rn(cover, (double)best);
+    }
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      float coll = 0.0f;
+#pragma unroll
+      for (int o = 0; o < NA; ++o) {
+        if (o == i) continue;
+        coll = fadd(coll, norm2(fsub(px[i], px[o]), fsub(py[i], py[o])) <= thr ? 1.0f : 0.0f);
+      }
+      __stcs(a.rew + i * B + e, (float)dsub_rn(-cover, (double)fmul(pen, coll)));
+    }
+  }
+  if (valid && (a.mode & SS_DO_DONE)) a.done[e] = (uint8_t)(steps >= a.ph.max_steps);
+  if (a.mode & SS_DO_OBS) {
+    float* sbuf = smem + (threadIdx.x >> 5) * (32 * O);
+    float* row = sbuf + (threadIdx.x & 31) * O;
+    const int64_t e0 = e - (threadIdx.x & 31);
+    const int nvalid = (int)min((int64_t)32, B - e0);
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      if (valid) {
+        row[0] = px[i]; row[1] = py[i]; row[2] = vx[i]; row[3] = vy[i];
+        int c = 4;
+#pragma unroll
+        for (int m = 0; m < NA; ++m) { row[c++] = fsub(mx[m], px[i]); row[c++] = fsub(my[m], py[i]); }
+#pragma unroll
+        for (int o = 0; o < NA; ++o) {
+          if (o == i) continue;
+          row[c++] = fsub(px[o], px[i]); row[c++] = fsub(py[o], py[i]);
+        }
+      }
+      if (nvalid > 0) warp_flush(a.obs + i * a.obs_stride + e0 * O, nvalid, O, sbuf);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// transport (scenarios/transport.py): NA agents (dyn 0..NA-1), package box
+// (entity NA, dyn row NA), goal marker (entity NA+1, stat row 0).
+// Pairs, lexicographic: for i: agents j>i (sphere-sphere), then (i, package)
+// (sphere-box).  sc[0] = box half length (as f32 of the python double) ,
+// sc[1] = half width, sc[2] = f32(success_dist); the doubles are passed via
+// si-packed bits: see make_small_args.
+// ---------------------------------------------------------------------------
+template <int NA>
+__global__ void __launch_bounds__(kSmallThreads) k_transport(const SmallArgs a) {
+  extern __shared__ __align__(16) float smem[];
+  if (a.guard && *a.guard) return;
+  constexpr int O = 12;
+  const int64_t B = a.s.B;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = e < B;
+  float px[NA + 1], py[NA + 1], vx[NA + 1], vy[NA + 1];
+  float gx = 0.f, gy = 0.f, prot = 0.f;
+  if (valid) {
+#pragma unroll
+    for (int i = 0; i <= NA; ++i) {
+      const float4 q = a.s.dyn[i * B + e];
+      px[i] = q.x; py[i] = q.y; vx[i] = q.z; vy[i] = q.w;
+    }
+    const float2 g = a.s.stat[e];
+    gx = g.x; gy = g.y;
+  }
+  if (valid && (a.mode & SS_DO_PHYSICS)) {
+    prot = a.s.rot[NA * B + e].x;
+    const float ca = cosf(prot), sa = sinf(prot);
+    const double hx = a.sd[0], hy = a.sd[1];
+    float fx[NA + 1], fy[NA + 1];
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      const SsEntityDesc& d = a.ents[i];
+      const float2 u = a.act[i][e];
+      fx[i] = decode_axis(u.x, d, a.raw_forces);
+      fy[i] = decode_axis(u.y, d, a.raw_forces);
+    }
+    fx[NA] = 0.0f; fy[NA] = 0.0f;
+    if (a.ph.has_gravity) {
+#pragma unroll
+      for (int i = 0; i <= NA; ++i) {
+        fx[i] = fadd(fx[i], a.ents[i].grav_x); fy[i] = fadd(fy[i], a.ents[i].grav_y);
+      }
+    }
+    int p = 0;
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+#pragma unroll
+      for (int j = i + 1; j < NA; ++j, ++p) {
+        const SsPairDesc pr = a.pairs[p];
+        float cx, cy;
+        if (contact_force(px[i], py[i], px[j], py[j], pr.d_min, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
+          fx[i] = fadd(fx[i], cx); fy[i] = fadd(fy[i], cy);
+          fx[j] = fsub(fx[j], cx); fy[j] = fsub(fy[j], cy);
+        }
+      }
+      {  // agent i vs package (sphere-box)
+        const SsPairDesc pr = a.pairs[p++];
+        float qx, qy, cx, cy;
+        closest_point_on_box(px[i], py[i], px[NA], py[NA], ca, sa, hx, hy, qx, qy);
+        if (contact_force(px[i], py[i], qx, qy, pr.d_min, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
+          fx[i] = fadd(fx[i], cx); fy[i] = fadd(fy[i], cy);
+          fx[NA] = fsub(fx[NA], cx); fy[NA] = fsub(fy[NA], cy);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i <= NA; ++i) {
+      const SsEntityDesc& d = a.ents[i];
+      integrate_lin(px[i], py[i], vx[i], vy[i], fx[i], fy[i], a.ph.keep, d.inv_m_dt, a.ph.dt,
+                    d.max_speed);
+      a.s.dyn[i * B + e] = make_float4(px[i], py[i], vx[i], vy[i]);
+    }
+  }
+  int64_t steps = 0;
+  if (valid && (a.mode & (SS_DO_COUNT | SS_DO_DONE))) {
+    steps = a.s.step_count[e];
+    if (a.mode & SS_DO_COUNT) { steps += 1; a.s.step_count[e] = steps; }
+  }
+  if (valid && (a.mode & (SS_DO_REWARD | SS_DO_DONE))) {
+    const float gap = norm2(fsub(px[NA], gx), fsub(py[NA], gy));
+    if (a.mode & SS_DO_REWARD) {
+#pragma unroll
+      for (int i = 0; i < NA; ++i) __stcs(a.rew + i * B + e, -gap);
+    }
+    if (a.mode & SS_DO_DONE) a.done[e] = (uint8_t)((gap < a.sc[2]) | (steps >= a.ph.max_steps));
+  }
+  if (a.mode & SS_DO_OBS) {
+    float* sbuf = smem + (threadIdx.x >> 5) * (32 * O);
+    float* row = sbuf + (threadIdx.x & 31) * O;
+    const int64_t e0 = e - (threadIdx.x & 31);
+    const int nvalid = (int)min((int64_t)32, B - e0);
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      if (valid) {
+        row[0] = px[i]; row[1] = py[i]; row[2] = vx[i]; row[3] = vy[i];
+        row[4] = fsub(px[NA], px[i]); row[5] = fsub(py[NA], py[i]);
+        row[6] = fsub(gx, px[i]); row[7] = fsub(gy, py[i]);
+        row[8] = fsub(px[NA], gx); row[9] = fsub(py[NA], gy);
+        row[10] = vx[NA]; row[11] = vy[NA];
+      }
+      if (nvalid > 0) warp_flush(a.obs + i * a.obs_stride + e0 * O, nvalid, O, sbuf);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// flocking (scenarios/flocking.py): NA agents (dyn 0..NA-1), beacon marker
+// (entity NA, stat row 0), NO rocks (entity NA+1+r, stat row 1+r, immovable).
+// Pairs, lexicographic: for i: agents j>i, then rocks.  Optional Lidar
+// (sensors.py) appended to the observation: n_rays ranges per agent.
+// sc[0] = f32 agent-agent touch threshold, sc[1] = agent-rock threshold,
+// sc[2] = f32(collision_penalty); si[4] = NO; sd[0], sd[1] = agent / rock
+// radius^2 as python doubles (sensors.py:47).
+// ---------------------------------------------------------------------------
+struct FlockLidarK {
+  double r2_agent, r2_rock;
+};
+
+template <int NA>
+__global__ void __launch_bounds__(kSmallThreads) k_flocking(const SmallArgs a, const FlockLidarK lk) {
+  extern __shared__ __align__(16) float smem[];
+  if (a.guard && *a.guard) return;
+  const int NO = a.si[4];
+  const int O = a.obs_dim;
+  const int64_t B = a.s.B;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = e < B;
+  float px[NA], py[NA], vx[NA], vy[NA];
+  float rx[kFlockMaxRocks], ry[kFlockMaxRocks];
+  float bx = 0.f, by = 0.f;
+  if (valid) {
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      const float4 q = a.s.dyn[i * B + e];
+      px[i] = q.x; py[i] = q.y; vx[i] = q.z; vy[i] = q.w;
+    }
+    const float2 bq = a.s.stat[e];
+    bx = bq.x; by = bq.y;
+#pragma unroll
+    for (int r = 0; r < kFlockMaxRocks; ++r) {
+      if (r < NO) { const float2 q = a.s.stat[(1 + r) * B + e]; rx[r] = q.x; ry[r] = q.y; }
+      else { rx[r] = 0.f; ry[r] = 0.f; }
+    }
+  }
+  if (valid && (a.mode & SS_DO_PHYSICS)) {
+    float fx[NA], fy[NA];
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      const SsEntityDesc& d = a.ents[i];
+      const float2 u = a.act[i][e];
+      fx[i] = decode_axis(u.x, d, a.raw_forces);
+      fy[i] = decode_axis(u.y, d, a.raw_forces);
+      if (a.ph.has_gravity) { fx[i] = fadd(fx[i], d.grav_x); fy[i] = fadd(fy[i], d.grav_y); }
+    }
+    int p = 0;
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+#pragma unroll
+      for (int j = i + 1; j < NA; ++j, ++p) {
+        const SsPairDesc pr = a.pairs[p];
+        float cx, cy;
+        if (contact_force(px[i], py[i], px[j], py[j], pr.d_min, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
+          fx[i] = fadd(fx[i], cx); fy[i] = fadd(fy[i], cy);
+          fx[j] = fsub(fx[j], cx); fy[j] = fsub(fy[j], cy);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < kFlockMaxRocks; ++r) {
+        if (r < NO) {
+          const SsPairDesc pr = a.pairs[p++];
+          float cx, cy;
+          if (contact_force(px[i], py[i], rx[r], ry[r], pr.d_min, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
+            fx[i] = fadd(fx[i], cx); fy[i] = fadd(fy[i], cy);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      const SsEntityDesc& d = a.ents[i];
+      integrate_lin(px[i], py[i], vx[i], vy[i], fx[i], fy[i], a.ph.keep, d.inv_m_dt, a.ph.dt,
+                    d.max_speed);
+      a.s.dyn[i * B + e] = make_float4(px[i], py[i], vx[i], vy[i]);
+    }
+  }
+  int64_t steps = 0;
+  if (valid && (a.mode & (SS_DO_COUNT | SS_DO_DONE))) {
+    steps = a.s.step_count[e];
+    if (a.mode & SS_DO_COUNT) { steps += 1; a.s.step_count[e] = steps; }
+  }
+  if (valid && (a.mode & SS_DO_REWARD)) {
+    const float thr_aa = a.sc[0], thr_ar = a.sc[1], pen = a.sc[2];
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      const float gap = norm2(fsub(px[i], bx), fsub(py[i], by));
+      float ca = 0.0f, cr = 0.0f;
+#pragma unroll
+      for (int o = 0; o < NA; ++o) {
+        if (o == i) continue;
+        ca = fadd(ca, norm2(fsub(px[i], px[o]), fsub(py[i], py[o])) <= thr_aa ? 1.0f : 0.0f);
+      }
+#pragma unroll
+      for (int r = 0; r < kFlockMaxRocks; ++r) {
+        if (r < NO) cr = fadd(cr, norm2(fsub(px[i], rx[r]), fsub(py[i], ry[r])) <= thr_ar ? 1.0f : 0.0f);
+      }
+      __stcs(a.rew + i * B + e, fsub(-gap, fmul(pen, fadd(ca, cr))));
+    }
+  }
+  if (valid && (a.mode & SS_DO_DONE)) a.done[e] = (uint8_t)(steps >= a.ph.max_steps);
+  if (a.mode & SS_DO_OBS) {
+    float* sbuf = smem + (threadIdx.x >> 5) * (32 * O);
+    float* row = sbuf + (threadIdx.x & 31) * O;
+    const int64_t e0 = e - (threadIdx.x & 31);
+    const int nvalid = (int)min((int64_t)32, B - e0);
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      if (valid) {
+        row[0] = px[i]; row[1] = py[i]; row[2] = vx[i]; row[3] = vy[i];
+        row[4] = fsub(bx, px[i]); row[5] = fsub(by, py[i]);
+        int c = 6;
+#pragma unroll
+        for (int r = 0; r < kFlockMaxRocks; ++r) {
+          if (r < NO) { row[c] = fsub(rx[r], px[i]); row[c + 1] = fsub(ry[r], py[i]); c += 2; }
+        }
+#pragma unroll
+        for (int o = 0; o < NA; ++o) {
+          if (o == i) continue;
+          row[c] = fsub(px[o], px[i]); row[c + 1] = fsub(py[o], py[i]); c += 2;
+        }
+        if (a.n_rays > 0) {
+          // lidar_scan (sensors.py:138-146): fp64 rays vs every collidable
+          // entity except the emitter; nearest hit, capped at max_range.
+          const double ox = (double)px[i], oy = (double)py[i];
+          const float rot_i = a.attach_rot ? a.s.rot[i * B + e].x : 0.0f;
+          for (int m = 0; m < a.n_rays; ++m) {
+            double dx, dy;
+            if (rot_i == 0.0f) { dx = a.ray_dir[2 * m]; dy = a.ray_dir[2 * m + 1]; }
+            else {
+              const double ang = dadd_rn(dadd_rn(a.ray_start, (double)m * a.ray_span / a.n_rays),
+                                      (double)rot_i);
+              sincos(ang, &dy, &dx);
+            }
+            double best = __longlong_as_double(0x7ff0000000000000LL);
+#pragma unroll
+            for (int o = 0; o < NA; ++o) {
+              if (o == i) continue;
+              best = fmin(best, ray_circle(ox, oy, dx, dy, (double)px[o], (double)py[o], lk.r2_agent));
+            }
+#pragma unroll
+            for (int r = 0; r < kFlockMaxRocks; ++r) {
+              if (r < NO) best = fmin(best, ray_circle(ox, oy, dx, dy, (double)rx[r], (double)ry[r], lk.r2_rock));
+            }
+            row[c + m] = (float)fmin(best, a.lidar_range);
+          }
+        }
+      }
+      if (nvalid > 0) warp_flush(a.obs + i * a.obs_stride + e0 * O, nvalid, O, sbuf);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host-side dispatch
+// ---------------------------------------------------------------------------
+int launch_small(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_t st) {
+  SmallArgs a;
+  memset(&a, 0, sizeof(a));
+  a.s = make_state(w, buf);
+  a.ph = make_phys(w);
+  a.ents = w.d_ents;
+  a.pairs = w.d_pairs;
+  const int NA = w.d.n_agents;
+  if (NA < 1 || NA > kSmallMaxAgents) {
+    set_error("fused kernel instantiated for 1.." + std::to_string(kSmallMaxAgents) + " agents");
+    return SS_ERR_UNSUPPORTED;
+  }
+  if (io->mode & SS_DO_PHYSICS) {
+    for (int i = 0; i < NA; ++i) a.act[i] = reinterpret_cast<const float2*>(io->actions[i]);
+  }
+  a.obs = io->obs;
+  a.obs_stride = io->obs_agent_stride;
+  a.rew = io->rew;
+  a.done = io->done;
+  a.mode = io->mode;
+  a.raw_forces = io->raw_forces;
+  a.obs_dim = w.d.obs_dim;
+  a.guard = io->guard;
+  memcpy(a.sc, w.d.sc, sizeof(a.sc));
+  memcpy(a.sd, w.d.sd, sizeof(a.sd));
+  memcpy(a.si, w.d.si, sizeof(a.si));
+  const int64_t B = w.d.batch;
+  const unsigned grid = (unsigned)((B + kSmallThreads - 1) / kSmallThreads);
+  const size_t shmem = (size_t)kSmallThreads * w.d.obs_dim * sizeof(float);
+  switch (w.d.scenario) {
+    case SS_SCN_SIMPLE_SPREAD: {
+#define SS_CASE(n) case n: k_simple_spread<n><<<grid, kSmallThreads, shmem, st>>>(a); break;
+      switch (NA) { SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) }
+#undef SS_CASE
+      break;
+    }
+    case SS_SCN_TRANSPORT: {
+#define SS_CASE(n) case n: k_transport<n><<<grid, kSmallThreads, shmem, st>>>(a); break;
+      switch (NA) { SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) }
+#undef SS_CASE
+      break;
+    }
+    case SS_SCN_FLOCKING: {
+      if (w.d.si[4] > kFlockMaxRocks) {
+        set_error("flocking fused kernel supports at most 6 obstacles");
+        return SS_ERR_UNSUPPORTED;
+      }
+      FlockLidarK lk;
+      lk.r2_agent = w.d.sd[0];
+      lk.r2_rock = w.d.sd[1];
+      a.n_rays = w.d.lidar_rays;
+      a.lidar_range = w.d.lidar_max_range;
+      a.attach_rot = w.d.lidar_attach_rotation;
+      a.ray_start = w.d.lidar_start;
+      a.ray_span = w.d.lidar_span;
+      a.ray_dir = w.d_lidar_dirs;
+#define SS_CASE(n) case n: k_flocking<n><<<grid, kSmallThreads, shmem, st>>>(a, lk); break;
+      switch (NA) { SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) }
+#undef SS_CASE
+      break;
+    }
+    default:
+      set_error("launch_small: not a small scenario");
+      return SS_ERR_SCENARIO;
+  }
+  return cuda_status(cudaGetLastError(), "fused step launch");
+}
+
+}  // namespace ss

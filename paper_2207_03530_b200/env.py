@@ -1,0 +1,405 @@
+"""Episode layer (swarmsim/env.py): Scenario hooks, action decoding, Env.
+
+Env.step for a built-in scenario is ONE fused device launch (plus an
+optional NaN scan when validate=True): decode -> world_step -> post_step ->
+step_count -> rewards -> dones -> observations, all inside the kernel, with
+outputs written to fresh device tensors.  User-defined scenarios (plain
+Scenario subclasses) run physics in the generic step kernel and their own
+Python hooks on device tensors.  There is no CPU path: an Env needs a CUDA
+device and the built library.
+
+VMAS-style aliases: make_env, Environment (= Env), Env.reset_at(mask).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .batching import DeviceRng, SeededRng, Vec2, default_device
+from .core import Agent, AgentAction, World
+from .errors import ContractViolation, NativeError
+
+
+class Scenario:
+    """Task definition (env.py:20-54).  Subclasses override the hooks."""
+
+    max_steps: int = 200
+
+    def make_world(self, batch_size: int, rng: SeededRng) -> World:
+        raise NotImplementedError
+
+    def reset_world_at(self, world: World, env_index: int | None = None) -> None:
+        raise NotImplementedError
+
+    def reward(self, agent: Agent, world: World) -> torch.Tensor:
+        raise NotImplementedError
+
+    def observation(self, agent: Agent, world: World) -> torch.Tensor:
+        raise NotImplementedError
+
+    def done(self, world: World) -> torch.Tensor:
+        return torch.zeros(world.batch_size, dtype=torch.bool, device=world.device)
+
+    def info(self, agent: Agent, world: World) -> dict:
+        return {}
+
+    def post_step(self, world: World) -> None:
+        pass
+
+    def heuristic_action(self, agent_index: int, obs):
+        raise NotImplementedError
+
+
+@dataclass(frozen=True)
+class ActionSpec:
+    mode: str
+    move_dim: int = 2
+    comm_dim: int = 0
+    n_move_choices: int = 5
+
+    @property
+    def flat_dim(self) -> int:
+        return self.move_dim + self.comm_dim
+
+
+def _to_device(raw, device) -> torch.Tensor:
+    if isinstance(raw, torch.Tensor):
+        return raw.to(device, non_blocking=True)
+    arr = np.asarray(raw)
+    return torch.from_numpy(np.ascontiguousarray(arr)).to(device, non_blocking=True)
+
+
+def decode_action(raw, spec: ActionSpec, agent: Agent, rng: SeededRng) -> AgentAction:
+    """Raw policy output -> AgentAction (env.py:71-145), on the agent's device."""
+    world = agent.state._world
+    B, dev = world.batch_size, world.device
+    t = _to_device(raw, dev)
+    if t.is_floating_point() and bool(torch.isnan(t).any()):
+        raise ContractViolation(f"action for '{agent.name}' contains NaN")
+    if spec.mode == "continuous":
+        if t.ndim == 1 and spec.comm_dim == 0 and tuple(t.shape) == (2,) and B == 1:
+            t = t.reshape(1, 2)
+        if tuple(t.shape) != (B, spec.flat_dim):
+            raise ContractViolation(
+                f"continuous action for '{agent.name}' has shape {tuple(t.shape)}, expected {(B, spec.flat_dim)}")
+        t = t.to(torch.float32)
+        u = float(np.float32(agent.u_range))
+        mv = torch.clamp(t[:, :2], -u, u) * float(np.float32(agent.u_multiplier))
+        fx, fy = mv[:, 0].clone(), mv[:, 1].clone()
+        comm = t[:, 2:].clone() if spec.comm_dim else None
+    elif spec.mode == "discrete":
+        if t.is_floating_point() or t.dtype == torch.bool:
+            raise ContractViolation(f"discrete action for '{agent.name}' must be integer")
+        if spec.comm_dim:
+            if tuple(t.shape) != (B, 2):
+                raise ContractViolation(f"discrete action for '{agent.name}' has shape {tuple(t.shape)}, expected {(B, 2)}")
+            move, cidx = t[:, 0], t[:, 1]
+        else:
+            if tuple(t.shape) == (B, 1):
+                t = t[:, 0]
+            if tuple(t.shape) != (B,):
+                raise ContractViolation(f"discrete action for '{agent.name}' has shape {tuple(t.shape)}, expected {(B,)}")
+            move, cidx = t, None
+        if bool(((move < 0) | (move >= spec.n_move_choices)).any()):
+            raise ContractViolation(
+                f"discrete move index for '{agent.name}' out of range [0, {spec.n_move_choices})")
+        u = float(np.float32(agent.u_range * agent.u_multiplier))
+        z = torch.zeros(B, device=dev)
+        fx = torch.where(move == 1, u, torch.where(move == 2, -u, z))
+        fy = torch.where(move == 3, u, torch.where(move == 4, -u, z))
+        if cidx is not None:
+            if bool(((cidx < 0) | (cidx >= spec.comm_dim)).any()):
+                raise ContractViolation(f"comm index for '{agent.name}' out of range [0, {spec.comm_dim})")
+            comm = torch.zeros((B, spec.comm_dim), device=dev)
+            comm[torch.arange(B, device=dev), cidx.long()] = 1.0
+        else:
+            comm = None
+    else:
+        raise ContractViolation(f"unknown action mode {spec.mode!r}")
+    if agent.action_noise_std > 0.0:
+        noise = torch.from_numpy(rng.normal(0.0, agent.action_noise_std, (B, 2))).to(dev)
+        fx = fx + noise[:, 0]
+        fy = fy + noise[:, 1]
+    if agent.silent:
+        comm = None
+    return AgentAction(force=Vec2(fx, fy), comm=comm)
+
+
+@dataclass
+class StepResult:
+    obs: list
+    rewards: list
+    dones: torch.Tensor
+    infos: list = field(default_factory=list)
+
+
+class Env:
+    """Batched episode driver around one scenario (env.py:156-235)."""
+
+    def __init__(self, scenario: Scenario, batch_size: int, seed: int = 0, max_steps: int | None = None,
+                 action_mode: str = "continuous", device=None, validate: bool = True,
+                 env_offset: int = 0, global_batch: int | None = None):
+        if batch_size < 1:
+            raise ContractViolation(f"batch_size must be >= 1, got {batch_size}")
+        if action_mode not in ("continuous", "discrete"):
+            raise ContractViolation(f"unknown action mode {action_mode!r}")
+        dev = torch.device(device) if device is not None else default_device()
+        if dev.type != "cuda":
+            raise NativeError("the batched step runs on a CUDA device only (no CPU implementation)")
+        N.lib()   # fail loudly now if the library is missing
+        self.scenario = scenario
+        self.batch_size = int(batch_size)
+        self.device = dev
+        self.validate = validate
+        with torch.cuda.device(dev):
+            self.rng = DeviceRng(seed, dev)
+            self.world = _make_world(scenario, batch_size, self.rng, dev)
+        self.world.rng = self.rng
+        gb = self.batch_size if global_batch is None else int(global_batch)
+        if env_offset < 0 or env_offset + self.batch_size > gb:
+            raise ContractViolation("shard [env_offset, env_offset + batch_size) outside global_batch")
+        self.world.env_offset = int(env_offset)
+        self.world.global_batch = gb
+        self.world._touch()
+        self._max_steps = max_steps if max_steps is not None else scenario.max_steps
+        self.world.max_steps = self._max_steps
+        self.action_mode = action_mode
+        self.action_specs = [ActionSpec(mode=action_mode, comm_dim=0 if a.silent else a.comm_dim)
+                             for a in self.world.agents]
+        self._flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.reset()
+
+    # -- properties ----------------------------------------------------------
+    @property
+    def agents(self) -> list[Agent]:
+        return self.world.agents
+
+    @property
+    def step_count(self) -> torch.Tensor:
+        return self.world.step_count
+
+    @property
+    def max_steps(self) -> int:
+        return self._max_steps
+
+    @max_steps.setter
+    def max_steps(self, v: int) -> None:
+        self._max_steps = int(v)
+        self.world.max_steps = self._max_steps
+        self.world._touch()
+
+    @property
+    def fused(self) -> bool:
+        return getattr(self.scenario, "native_id", None) is not None
+
+    # -- reset ---------------------------------------------------------------
+    def reset(self, env_index: int | None = None) -> list:
+        """Reset every env, or one index, and return fresh observations (env.py:189-198)."""
+        if env_index is not None and not (0 <= env_index < self.batch_size):
+            raise ContractViolation(f"env_index {env_index} out of range [0, {self.batch_size})")
+        self.scenario.reset_world_at(self.world, env_index)
+        if env_index is None:
+            self.world.step_count.zero_()
+        else:
+            self.world.step_count[env_index] = 0
+        return self.observations()
+
+    def reset_at(self, mask) -> list:
+        """Reset the selected envs (bool mask (B,), index, or index list).
+
+        Equivalent — bitwise, including the random stream — to calling
+        reset(env_index=i) for each selected i in ascending order; for the
+        built-in scenarios it is one masked reset launch.
+        """
+        m = _as_mask(mask, self.batch_size, self.device)
+        if self.fused:
+            self.scenario.reset_world_masked(self.world, m)
+        else:
+            for i in torch.nonzero(m).flatten().tolist():
+                self.scenario.reset_world_at(self.world, i)
+                self.world.step_count[i] = 0
+        return self.observations()
+
+    def observations(self) -> list:
+        if self.fused:
+            obs = self.scenario.observe_all(self.world)
+        else:
+            obs = [self.scenario.observation(a, self.world).to(torch.float32) for a in self.agents]
+        return self._obs_noise(obs)
+
+    def _obs_noise(self, obs: list) -> list:
+        out = []
+        for agent, o in zip(self.agents, obs):
+            if agent.obs_noise_std > 0.0:
+                o = o + torch.from_numpy(self.rng.normal(0.0, agent.obs_noise_std, tuple(o.shape))).to(o.device)
+            out.append(o)
+        return out
+
+    # -- step ----------------------------------------------------------------
+    def step(self, raw_actions) -> StepResult:
+        """Advance the whole batch one step (env.py:209-235)."""
+        agents = self.agents
+        if isinstance(raw_actions, torch.Tensor) and raw_actions.ndim == 3:
+            raw_actions = list(raw_actions.unbind(0))
+        if len(raw_actions) != len(agents):
+            raise ContractViolation(f"got {len(raw_actions)} actions for {len(agents)} agents")
+        for raw, agent in zip(raw_actions, agents):
+            if raw is None and agent.action_script is None:
+                raise ContractViolation(f"agent '{agent.name}' needs an action, got None")
+        if self.fused:
+            return self._step_fused(raw_actions)
+        return self._step_generic(raw_actions)
+
+    def _fast_actions(self, raw_actions):
+        """Continuous, noiseless, unscripted: raw (B, 2) device tensors, no decode on host."""
+        B, dev = self.batch_size, self.device
+        out = []
+        for raw, agent, spec in zip(raw_actions, self.agents, self.action_specs):
+            t = _to_device(raw, dev)
+            if t.ndim == 1 and spec.comm_dim == 0 and tuple(t.shape) == (2,) and B == 1:
+                t = t.reshape(1, 2)
+            if tuple(t.shape) != (B, spec.flat_dim):
+                raise ContractViolation(
+                    f"continuous action for '{agent.name}' has shape {tuple(t.shape)}, expected {(B, spec.flat_dim)}")
+            if spec.comm_dim:
+                if not agent.silent:
+                    self.world.comm[agent.name] = t[:, 2:].to(torch.float32).clone()
+                t = t[:, :2]
+            if t.dtype != torch.float32:
+                t = t.to(torch.float32)
+            out.append(t.contiguous())
+        return out
+
+    def _host_decoded(self, raw_actions):
+        """Discrete / noisy / scripted agents: final forces computed on device with torch."""
+        forces = []
+        for raw, agent, spec in zip(raw_actions, self.agents, self.action_specs):
+            if raw is None:
+                act = agent.action_script(agent, self.world)
+            else:
+                act = decode_action(raw, spec, agent, self.rng)
+            from .dynamics import _validate_action
+
+            _validate_action(agent, act, self.batch_size)
+            agent.action = act
+            if not agent.silent and act.comm is not None:
+                self.world.comm[agent.name] = act.comm
+            forces.append(torch.stack([act.force.x, act.force.y], 1).to(self.device, torch.float32).contiguous())
+        return forces
+
+    def _needs_host_decode(self, raw_actions) -> bool:
+        if self.action_mode != "continuous":
+            return True
+        for raw, agent in zip(raw_actions, self.agents):
+            if raw is None or agent.action_script is not None or agent.action_noise_std > 0.0:
+                return True
+        return False
+
+    def _step_fused(self, raw_actions) -> StepResult:
+        world, sc = self.world, self.scenario
+        raw = self._needs_host_decode(raw_actions)
+        forces = self._host_decoded(raw_actions) if raw else self._fast_actions(raw_actions)
+        guard = None
+        if self.validate and not raw:
+            self._flag.zero_()
+            h = sc.native_handle(world)
+            N.check(N.lib().ss_check_actions(h.handle, N.pointer_array(forces), N.ptr(self._flag),
+                                             N.stream_handle(self.device)))
+            guard = self._flag
+        obs, rew, done = sc.launch(world, N.MODE_STEP, forces=forces, raw_forces=raw, guard=guard)
+        if guard is not None and int(self._flag.item()) != 0:
+            bad = next(a.name for a, f in zip(self.agents, forces) if bool(torch.isnan(f).any()))
+            raise ContractViolation(f"action for '{bad}' contains NaN")
+        obs_list = self._obs_noise([obs[a, : self.batch_size] for a in range(len(self.agents))])
+        infos = [sc.info(a, world) for a in self.agents]
+        return StepResult(obs=obs_list, rewards=list(rew.unbind(0)), dones=done, infos=infos)
+
+    def _step_generic(self, raw_actions) -> StepResult:
+        from .dynamics import run_world_step
+
+        world, sc = self.world, self.scenario
+        forces = self._host_decoded(raw_actions)
+        run_world_step(world, forces, decode_mask=0, count=False)
+        sc.post_step(world)
+        world.step_count += 1
+        rewards = [torch.as_tensor(sc.reward(a, world), device=self.device).to(torch.float32) for a in self.agents]
+        dones = torch.as_tensor(sc.done(world), device=self.device).to(torch.bool) | (world.step_count >= self.max_steps)
+        obs = self.observations()
+        infos = [sc.info(a, world) for a in self.agents]
+        return StepResult(obs=obs, rewards=rewards, dones=dones, infos=infos)
+
+
+Environment = Env
+
+
+def _make_world(scenario: Scenario, batch_size: int, rng, device) -> World:
+    w = scenario.make_world(batch_size, rng)
+    if w.device != device:
+        raise ContractViolation(f"scenario built its world on {w.device}, Env runs on {device}")
+    return w
+
+
+def _as_mask(mask, B: int, device) -> torch.Tensor:
+    if isinstance(mask, (int, np.integer)):
+        idx = [int(mask)]
+    elif isinstance(mask, torch.Tensor) and mask.dtype == torch.bool:
+        if tuple(mask.shape) != (B,):
+            raise ContractViolation(f"reset mask must have shape ({B},), got {tuple(mask.shape)}")
+        return mask.to(device)
+    else:
+        arr = np.asarray(mask.cpu() if isinstance(mask, torch.Tensor) else mask)
+        if arr.dtype == bool:
+            if arr.shape != (B,):
+                raise ContractViolation(f"reset mask must have shape ({B},), got {arr.shape}")
+            return torch.from_numpy(arr).to(device)
+        idx = [int(i) for i in arr.reshape(-1)]
+    for i in idx:
+        if not (0 <= i < B):
+            raise ContractViolation(f"env_index {i} out of range [0, {B})")
+    m = torch.zeros(B, dtype=torch.bool)
+    m[idx] = True
+    return m.to(device)
+
+
+class SingleEnv:
+    """Unbatched facade over a batch_size=1 Env (env.py:238-266)."""
+
+    def __init__(self, env: Env):
+        if env.batch_size != 1:
+            raise ContractViolation("SingleEnv requires a batch_size=1 Env")
+        self.env = env
+
+    @property
+    def agents(self):
+        return self.env.agents
+
+    def reset(self, **kwargs):
+        return [o[0] for o in self.env.reset(**kwargs)]
+
+    def step(self, raw_actions):
+        batched = []
+        for raw, spec in zip(raw_actions, self.env.action_specs):
+            if raw is None:
+                batched.append(None)
+            elif spec.mode == "discrete":
+                batched.append(np.asarray(raw).reshape(1, -1) if np.ndim(raw) else np.asarray([raw]))
+            else:
+                batched.append(np.asarray(raw, dtype=np.float32).reshape(1, -1))
+        res = self.env.step(batched)
+        obs = [o[0] for o in res.obs]
+        rewards = [float(r[0]) for r in res.rewards]
+        return obs, rewards, bool(res.dones[0]), res.infos
+
+
+def make_env(scenario, num_envs: int = 32, device=None, continuous_actions: bool = True,
+             max_steps: int | None = None, seed: int | None = None, validate: bool = True, **kwargs) -> Env:
+    """VMAS-style constructor: make_env("simple_spread", num_envs=1_000_000, n_agents=3)."""
+    from .scenarios import create_scenario
+
+    sc = create_scenario(scenario, **kwargs) if isinstance(scenario, str) else scenario
+    return Env(sc, num_envs, seed=0 if seed is None else seed, max_steps=max_steps,
+               action_mode="continuous" if continuous_actions else "discrete", device=device,
+               validate=validate)

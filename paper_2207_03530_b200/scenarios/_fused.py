@@ -1,0 +1,190 @@
+"""Base class of the built-in scenarios whose whole step is one fused kernel.
+
+A FusedScenario keeps the reference's Scenario hooks (make_world,
+reset_world_at, reward, observation, done, post_step) but every hook is a
+launch of the scenario's fused kernel in the matching mode (SS_DO_* flags),
+so there is exactly one implementation of each task's semantics: the CUDA
+one.  Subclasses describe the task to the library through native_desc():
+scenario id, constants (rounded exactly as numpy rounds them), observation
+width, flag words and the reset program.
+
+If a world no longer matches the kernel's compiled pair enumeration (a
+user flipped a collidable / movable flag, swapped a shape, ...), the physics
+part runs in the generic world_step kernel and the fused kernel does the
+rest of the step (post_step, rewards, dones, observations).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from .. import _native as N
+from ..core import World
+from ..env import Scenario
+
+
+class FusedScenario(Scenario):
+    native_id: int | None = None
+    advances_rng_per_step = False   # discovery draws relocations every step
+
+    # ---- subclass interface -------------------------------------------------
+    def obs_dim(self, world: World) -> int:
+        raise NotImplementedError
+
+    def n_flag_words(self) -> int:
+        return 0
+
+    def reset_ops(self, world: World) -> list:
+        """[(entity_index, "scatter", (lo_x, lo_y), (hi_x, hi_y)) | (k, "place", (x, y), None)]."""
+        raise NotImplementedError
+
+    def template_pairs(self, world: World) -> list:
+        """Pair list the fused kernel enumerates (must equal the world's)."""
+        raise NotImplementedError
+
+    def fill_constants(self, world: World, d: "N.SsWorldDesc") -> None:
+        pass
+
+    def template_ok(self, world: World) -> bool:
+        return True
+
+    # ---- descriptor ---------------------------------------------------------
+    def native_desc(self, world: World) -> "N.SsWorldDesc":
+        d = world.base_desc(self.native_id, getattr(world, "max_steps", self.max_steps))
+        d.obs_dim = self.obs_dim(world)
+        d.n_flag_words = world.flags.shape[0]
+        ops = self.reset_ops(world)
+        arr = (N.SsResetOp * max(1, len(ops)))()
+        for n, (k, kind, lo, hi) in enumerate(ops):
+            arr[n].entity = k
+            if kind == "scatter":
+                lo64 = np.asarray(lo, dtype=np.float64)
+                hi64 = np.asarray(hi, dtype=np.float64)
+                arr[n].kind = 0
+                arr[n].lo_x, arr[n].lo_y = float(lo64[0]), float(lo64[1])
+                arr[n].range_x = float(hi64[0] - lo64[0])
+                arr[n].range_y = float(hi64[1] - lo64[1])
+            else:
+                arr[n].kind = 1
+                arr[n].lo_x, arr[n].lo_y = float(lo[0]), float(lo[1])
+        d.reset_ops = ctypes.cast(arr, ctypes.POINTER(N.SsResetOp))
+        d.n_reset_ops = len(ops)
+        self.fill_constants(world, d)
+        d._keep = (d._keep, arr)
+        return d
+
+    def native_handle(self, world: World):
+        world.ensure_flag_words(self.n_flag_words())
+        return world.native(("fused", world.version), lambda: self.native_desc(world))
+
+    def physics_fused(self, world: World) -> bool:
+        key = ("tmpl", world.version)
+        ok = world._native_cache.get(key)
+        if ok is None:
+            ok = _Flag(self.template_ok(world) and
+                       list(world.collidable_pairs()) == list(self.template_pairs(world)))
+            world._native_cache[key] = ok
+        return ok.value
+
+    # ---- launches -------------------------------------------------------------
+    def alloc_outputs(self, world: World, obs_dim: int):
+        A, B = len(world.agents), world.batch_size
+        bp = B
+        while (bp * obs_dim) % 4:
+            bp += 1
+        obs = torch.empty((A, bp, obs_dim), device=world.device)
+        rew = torch.empty((A, B), device=world.device)
+        done = torch.empty(B, dtype=torch.bool, device=world.device)
+        return obs, rew, done
+
+    def launch(self, world: World, mode: int, forces=None, raw_forces: bool = False, guard=None,
+               flip_rng: bool = True):
+        """One fused launch in `mode`; returns (obs (A, Bp, O), rew (A, B), done (B,))."""
+        world.ensure_device_rng()
+        h = self.native_handle(world)
+        dev = world.device
+        st = N.stream_handle(dev)
+        if (mode & N.DO_PHYSICS) and not self.physics_fused(world):
+            from ..dynamics import run_world_step
+
+            run_world_step(world, forces, decode_mask=0 if raw_forces else (1 << 256) - 1, count=False)
+            mode &= ~N.DO_PHYSICS
+        obs, rew, done = self.alloc_outputs(world, h.obs_dim)
+        io = N.SsStepIO()
+        ptrs = N.pointer_array(forces or [])
+        io.actions = ptrs
+        io.obs = N.ptr(obs)
+        io.obs_agent_stride = obs.shape[1] * obs.shape[2]
+        io.rew = N.ptr(rew)
+        io.done = N.ptr(done)
+        io.mode = mode
+        io.guard = N.ptr(guard)
+        io.raw_forces = int(raw_forces)
+        buf = world.buffers()
+        N.check(N.lib().ss_env_step(h.handle, ctypes.byref(buf), ctypes.byref(io), st))
+        if flip_rng and (mode & N.DO_POST) and self.advances_rng_per_step:
+            world.rng.flip()
+        return obs, rew, done
+
+    # ---- reference hooks as kernel modes ----------------------------------
+    def observe_all(self, world: World) -> list:
+        obs, _, _ = self.launch(world, N.DO_OBS)
+        return [obs[a, : world.batch_size] for a in range(obs.shape[0])]
+
+    def observation(self, agent, world: World) -> torch.Tensor:
+        return self.observe_all(world)[world.agents.index(agent)]
+
+    def reward(self, agent, world: World) -> torch.Tensor:
+        _, rew, _ = self.launch(world, N.DO_REWARD)
+        return rew[world.agents.index(agent)]
+
+    def done(self, world: World) -> torch.Tensor:
+        # scenario termination only: the horizon term is Env's (env.py:232)
+        saved = getattr(world, "max_steps", self.max_steps)
+        try:
+            world.max_steps = 2**62
+            world._drop_native()
+            _, _, done = self.launch(world, N.DO_DONE)
+        finally:
+            world.max_steps = saved
+            world._drop_native()
+        return done
+
+    def post_step(self, world: World) -> None:
+        self.launch(world, N.DO_POST)
+
+    def reset_world_at(self, world: World, env_index: int | None = None) -> None:
+        if env_index is None:
+            self._reset(world, None)
+        else:
+            m = torch.zeros(world.batch_size, dtype=torch.bool, device=world.device)
+            m[env_index] = True
+            self._reset(world, m)
+
+    def reset_world_masked(self, world: World, mask: torch.Tensor, mask_base=None, mask_total=None) -> None:
+        self._reset(world, mask, mask_base, mask_total)
+
+    def _reset(self, world: World, mask, mask_base=None, mask_total=None) -> None:
+        world.ensure_device_rng()
+        h = self.native_handle(world)
+        buf = world.buffers()
+        m = None if mask is None else mask.to(world.device, torch.uint8).contiguous()
+        N.check(N.lib().ss_reset(h.handle, ctypes.byref(buf), N.ptr(m), N.ptr(mask_base),
+                                 N.ptr(mask_total), N.stream_handle(world.device)))
+        world.rng.flip()
+
+
+class _Flag:
+    """Cache entry with a close() so World._drop_native can clear it."""
+
+    def __init__(self, value: bool):
+        self.value = bool(value)
+
+    def close(self) -> None:
+        pass
+
+
+def f32(x) -> float:
+    return float(np.float32(x))
