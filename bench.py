@@ -71,24 +71,37 @@ def peaks() -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle sampling during the timed region."""
+    """nvidia-smi clocks / throttle reasons, sampled every 50 ms by a reader
+    thread for as long as the context is open (soak + warm-up + timed steps)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-        self.path = Path(os.environ.get("TMPDIR", "/tmp")) / f"bench_clocks_{os.getpid()}.csv"
+        self.rows: list[list[str]] = []
+        self.error = None
+
+    def _reader(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7 and parts[0].isdigit():
+                self.rows.append(parts)
 
     def __enter__(self):
+        import threading
+
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}",
-                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-        except (FileNotFoundError, OSError):
-            self.proc = None
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True, bufsize=1)
+            self.thread = threading.Thread(target=self._reader, daemon=True)
+            self.thread.start()
+        except (FileNotFoundError, OSError) as exc:
+            self.proc, self.error = None, str(exc)
         return self
 
     def __exit__(self, *exc):
@@ -98,15 +111,12 @@ class ClockSampler:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+            self.thread.join(timeout=2)
 
     def summary(self) -> dict:
-        if self.proc is None or not self.path.exists():
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        rows = []
-        for line in self.path.read_text().splitlines():
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 7 and parts[0].isdigit():
-                rows.append(parts)
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [f"nvidia-smi unavailable: {self.error}"]}
+        rows = list(self.rows)
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
         import statistics
@@ -118,8 +128,8 @@ class ClockSampler:
             for n, v in zip(names, r[3:7]):
                 if v.lower() == "active":
                     reasons.add(n)
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": int(rows[0][1]), "reasons": sorted(reasons),
-                "samples": len(rows)}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": int(rows[0][1]),
+                "reasons": sorted(reasons), "samples": len(rows)}
 
 
 def dist_setup(n_gpus: int):
@@ -238,23 +248,33 @@ def run_b200(args, rank, world, local) -> None:
     K, W = args.steps, args.warmup
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
-    acts = [torch.rand((A, B, 2), device=dev, generator=gen).mul_(2.0).sub_(1.0) for _ in range(K + W)]
-    acts = [list(a.unbind(0)) for a in acts]
+    # a pool of distinct action sets, cycled; the pool spans > 2x L2 so no
+    # step reads actions another recent step left in L2
+    set_bytes = A * B * 8
+    pool = max(2, min(K + W, -(-2 * 126_000_000 // set_bytes)))
+    acts = [torch.rand((A, B, 2), device=dev, generator=gen).mul_(2.0).sub_(1.0) for _ in range(pool)]
     stream = torch.cuda.current_stream(dev)
 
     # ---- kernel-path throughput (device-resident inputs) -------------------
-    for t in range(W):
-        env.step(acts[t])
-    barrier(world, dev)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     with ClockSampler(dev.index) as clocks:
+        # clock soak: untimed steps so nvidia-smi sees the loaded clocks
+        t_soak, n = time.perf_counter(), 0
+        while time.perf_counter() - t_soak < args.soak:
+            env.step(acts[n % pool])
+            n += 1
+            if n % 64 == 0:
+                torch.cuda.synchronize(dev)
+        for t in range(W):
+            env.step(acts[t % pool])
+        barrier(world, dev)
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
         for k in range(K):
             starts[k].record(stream)
-            env.step(acts[W + k])
+            env.step(acts[(W + k) % pool])
             ends[k].record(stream)
         t1.record(stream)
         torch.cuda.synchronize(dev)
@@ -325,6 +345,7 @@ def run_b200(args, rank, world, local) -> None:
             "e2e": {"value": e2e_value, "unit": "agent-steps/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": K,
+            "clock_soak_s": args.soak,
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,
         }
@@ -342,6 +363,7 @@ def main() -> None:
     ap.add_argument("--cpu-envs", type=int, default=1_000_000)
     ap.add_argument("--cpu-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--soak", type=float, default=1.5, help="seconds of untimed steps for clock sampling")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

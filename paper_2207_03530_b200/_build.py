@@ -60,9 +60,10 @@ def needs_build() -> bool:
     return any(p.stat().st_mtime > t for p in sources() + _headers() + [Path(__file__)])
 
 
-def _compile(nvcc: str, src: Path, verbose: bool) -> Path:
-    obj = OBJ_DIR / (src.stem + ".o")
-    cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-I", str(INCLUDE), "-c", str(src), "-o", str(obj)]
+def _compile(nvcc: str, src: Path, verbose: bool, defines=(), obj_dir: Path = OBJ_DIR) -> Path:
+    obj = obj_dir / (src.stem + ".o")
+    cmd = [nvcc, *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", str(INCLUDE), "-c", str(src),
+           "-o", str(obj)]
     if verbose:
         cmd += ["-Xptxas", "-v"]
     res = subprocess.run(cmd, capture_output=True, text=True)
@@ -73,22 +74,27 @@ def _compile(nvcc: str, src: Path, verbose: bool) -> Path:
     return obj
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile csrc/*.cu for sm_100a and link the shared library; returns its path."""
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, defines=(), out: Path | None = None) -> Path:
+    """Compile csrc/*.cu for sm_100a and link the shared library; returns its path.
+
+    defines / out: tuning variants (e.g. SS_SMALL_MINB=8) built beside the default library.
+    """
+    lib = out or LIB
+    if not force and not defines and out is None and not needs_build():
         return LIB
     nvcc = nvcc_path()
-    OBJ_DIR.mkdir(exist_ok=True)
+    obj_dir = OBJ_DIR if not defines else OBJ_DIR / "_".join(d.replace("=", "") for d in defines)
+    obj_dir.mkdir(parents=True, exist_ok=True)
     srcs = sources()
     with cf.ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
-        objs = list(ex.map(lambda s: _compile(nvcc, s, verbose), srcs))
-    tmp = LIB.with_suffix(".so.tmp")
+        objs = list(ex.map(lambda s: _compile(nvcc, s, verbose, defines, obj_dir), srcs))
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 def main() -> None:

@@ -14,7 +14,7 @@ from pathlib import Path
 
 from .errors import ContractViolation, NativeError, UnknownScenario, UnsupportedShapePair
 
-LIB_PATH = Path(__file__).resolve().parent / "libswarmsim_b200.so"
+LIB_PATH = Path(os.environ.get("SS_LIB_PATH") or Path(__file__).resolve().parent / "libswarmsim_b200.so")
 ABI_VERSION = 1
 RNG_WORDS = 12
 

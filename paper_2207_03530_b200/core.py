@@ -313,6 +313,7 @@ class World:
         self.aux = torch.zeros(self.batch_size, dtype=torch.float32, device=self.device)
         self.version = 0
         self._native_cache: dict = {}
+        self._buf_cache = None
 
     # -- entity bookkeeping ---------------------------------------------------
     @property
@@ -446,6 +447,7 @@ class World:
     def ensure_flag_words(self, n: int) -> None:
         if self.flags.shape[0] < max(1, n):
             self.flags = torch.zeros((max(1, n), self.batch_size), dtype=torch.int32, device=self.device)
+            self._touch()
 
     def entity_descs(self):
         p = self.params
@@ -530,6 +532,18 @@ class World:
             b.rng_cur = rng.cur
         return b
 
+    def buffers_ref(self):
+        """ctypes byref of a cached SsBuffers (rebuilt when buffers move)."""
+        c = self._buf_cache
+        if c is None or c[0] != self.version or c[3] is not self.rng:
+            b = self.buffers()
+            c = (self.version, b, ctypes.byref(b), self.rng)
+            self._buf_cache = c
+        b = c[1]
+        if isinstance(self.rng, DeviceRng):
+            b.rng_cur = self.rng.cur
+        return c[2]
+
     def ensure_device_rng(self) -> DeviceRng:
         """Promote the world's SeededRng to a device-backed stream (same state)."""
         if not isinstance(self.rng, DeviceRng):
@@ -548,6 +562,11 @@ class NativeWorld:
         self.handle = h
         self.obs_dim = desc.obs_dim
         self.scenario = desc.scenario
+        # reusable per-call argument block (the library copies it at launch)
+        self.act_ptrs = (ctypes.c_void_p * max(1, desc.n_agents))()
+        self.io = N.SsStepIO()
+        self.io.actions = self.act_ptrs
+        self.io_ref = ctypes.byref(self.io)
 
     def close(self) -> None:
         if self.handle:

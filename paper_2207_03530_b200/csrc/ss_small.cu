@@ -18,6 +18,10 @@ namespace ss {
 constexpr int kSmallMaxAgents = 8;
 constexpr int kFlockMaxRocks = 6;
 constexpr int kSmallThreads = 128;
+// minimum resident CTAs per SM requested from ptxas (register budget)
+#ifndef SS_SMALL_MINB
+#define SS_SMALL_MINB 1
+#endif
 
 struct SmallArgs {
   DevState s;
@@ -89,7 +93,7 @@ SS_DEV double ray_circle(double ox, double oy, double dx, double dy, double cx, 
 // sc[0] = f32 touching threshold (r_a + r_b), sc[1] = f32(collision_penalty)
 // ---------------------------------------------------------------------------
 template <int NA>
-__global__ void __launch_bounds__(kSmallThreads) k_simple_spread(const SmallArgs a) {
+__global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_simple_spread(const SmallArgs a) {
   extern __shared__ __align__(16) float smem[];
   if (a.guard && *a.guard) return;
   constexpr int O = 4 * NA + 2;
@@ -196,7 +200,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_simple_spread(const SmallArgs
 // si-packed bits: see make_small_args.
 // ---------------------------------------------------------------------------
 template <int NA>
-__global__ void __launch_bounds__(kSmallThreads) k_transport(const SmallArgs a) {
+__global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_transport(const SmallArgs a) {
   extern __shared__ __align__(16) float smem[];
   if (a.guard && *a.guard) return;
   constexpr int O = 12;
@@ -216,7 +220,8 @@ __global__ void __launch_bounds__(kSmallThreads) k_transport(const SmallArgs a) 
   }
   if (valid && (a.mode & SS_DO_PHYSICS)) {
     prot = a.s.rot[NA * B + e].x;
-    const float ca = cosf(prot), sa = sinf(prot);
+    float ca, sa;
+    if (prot == 0.0f) { ca = 1.0f; sa = prot; } else { sincosf(prot, &sa, &ca); }
     const double hx = a.sd[0], hy = a.sd[1];
     float fx[NA + 1], fy[NA + 1];
 #pragma unroll
@@ -309,7 +314,7 @@ struct FlockLidarK {
 };
 
 template <int NA>
-__global__ void __launch_bounds__(kSmallThreads) k_flocking(const SmallArgs a, const FlockLidarK lk) {
+__global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_flocking(const SmallArgs a, const FlockLidarK lk) {
   extern __shared__ __align__(16) float smem[];
   if (a.guard && *a.guard) return;
   const int NO = a.si[4];

@@ -92,15 +92,20 @@ def physics_world(world: World):
     return world.native(("physics", world.version), lambda: world.base_desc())
 
 
-def run_world_step(world: World, forces: list, decode_mask: int, count: bool) -> None:
-    """Launch the generic step kernel. forces[a]: (B, 2) f32 device tensor or None."""
+def run_world_step(world: World, forces: list, decode_mask: int, count: bool, stream=None) -> None:
+    """Launch the generic step kernel.
+
+    forces[a]: agent a's (B, 2) f32 device tensor, or its data pointer (int).
+    decode_mask bit a: apply decode_action's clip * u_multiplier on device.
+    """
     h = physics_world(world)
-    ptrs = N.pointer_array(forces)
+    ptrs = (ctypes.c_void_p * max(1, len(forces)))()
+    for i, f in enumerate(forces):
+        ptrs[i] = f if isinstance(f, int) else (None if f is None else f.data_ptr())
     mask = (ctypes.c_uint64 * 4)(*[(decode_mask >> (64 * i)) & (2**64 - 1) for i in range(4)])
     status = torch.zeros(1, dtype=torch.int32, device=world.device)
-    buf = world.buffers()
-    N.check(N.lib().ss_world_step(h.handle, ctypes.byref(buf), ptrs, mask, int(count), N.ptr(status),
-                                  N.stream_handle(world.device)))
+    st = stream if stream is not None else N.stream_handle(world.device)
+    N.check(N.lib().ss_world_step(h.handle, world.buffers_ref(), ptrs, mask, int(count), N.ptr(status), st))
 
 
 def world_step(world: World, actions: list) -> None:

@@ -240,9 +240,19 @@ class Env:
 
     # -- step ----------------------------------------------------------------
     def step(self, raw_actions) -> StepResult:
-        """Advance the whole batch one step (env.py:209-235)."""
+        """Advance the whole batch one step (env.py:209-235).
+
+        raw_actions: one (B, 2 + comm_dim) array/tensor per agent (None for
+        scripted agents), or a single (A, B, 2) tensor — the zero-copy fast path.
+        """
         agents = self.agents
         if isinstance(raw_actions, torch.Tensor) and raw_actions.ndim == 3:
+            if (self.fused and raw_actions.device == self.device and raw_actions.dtype == torch.float32
+                    and tuple(raw_actions.shape) == (len(agents), self.batch_size, 2)
+                    and raw_actions.is_contiguous() and not self._needs_host_decode([0] * len(agents))
+                    and all(s.comm_dim == 0 for s in self.action_specs)):
+                base, stride = raw_actions.data_ptr(), self.batch_size * 8
+                return self._step_fused_ptrs([base + a * stride for a in range(len(agents))], raw_actions, False)
             raw_actions = list(raw_actions.unbind(0))
         if len(raw_actions) != len(agents):
             raise ContractViolation(f"got {len(raw_actions)} actions for {len(agents)} agents")
@@ -299,23 +309,41 @@ class Env:
         return False
 
     def _step_fused(self, raw_actions) -> StepResult:
-        world, sc = self.world, self.scenario
         raw = self._needs_host_decode(raw_actions)
         forces = self._host_decoded(raw_actions) if raw else self._fast_actions(raw_actions)
+        return self._step_fused_ptrs([f.data_ptr() for f in forces], forces, raw)
+
+    def _step_fused_ptrs(self, ptrs, keepalive, raw: bool) -> StepResult:
+        world, sc = self.world, self.scenario
+        st = torch.cuda.current_stream(self.device).cuda_stream
         guard = None
         if self.validate and not raw:
             self._flag.zero_()
             h = sc.native_handle(world)
-            N.check(N.lib().ss_check_actions(h.handle, N.pointer_array(forces), N.ptr(self._flag),
-                                             N.stream_handle(self.device)))
+            arr = (N.c_vp * max(1, len(ptrs)))(*ptrs)
+            N.check(N.lib().ss_check_actions(h.handle, arr, self._flag.data_ptr(), st))
             guard = self._flag
-        obs, rew, done = sc.launch(world, N.MODE_STEP, forces=forces, raw_forces=raw, guard=guard)
+        obs, rew, done = sc.launch(world, N.MODE_STEP, action_ptrs=ptrs, raw_forces=raw, guard=guard,
+                                   flip_rng=False, stream=st)
         if guard is not None and int(self._flag.item()) != 0:
+            forces = keepalive if isinstance(keepalive, list) else list(keepalive.unbind(0))
             bad = next(a.name for a, f in zip(self.agents, forces) if bool(torch.isnan(f).any()))
             raise ContractViolation(f"action for '{bad}' contains NaN")
-        obs_list = self._obs_noise([obs[a, : self.batch_size] for a in range(len(self.agents))])
-        infos = [sc.info(a, world) for a in self.agents]
+        if sc.advances_rng_per_step:
+            world.rng.flip()
+        B = self.batch_size
+        obs_list = list((obs if obs.shape[1] == B else obs[:, :B]).unbind(0))
+        if self._any_obs_noise:
+            obs_list = self._obs_noise(obs_list)
+        if type(sc).info is _BASE_INFO:
+            infos = [{} for _ in self.agents]
+        else:
+            infos = [sc.info(a, world) for a in self.agents]
         return StepResult(obs=obs_list, rewards=list(rew.unbind(0)), dones=done, infos=infos)
+
+    @property
+    def _any_obs_noise(self) -> bool:
+        return any(a.obs_noise_std > 0.0 for a in self.agents)
 
     def _step_generic(self, raw_actions) -> StepResult:
         from .dynamics import run_world_step
@@ -333,6 +361,7 @@ class Env:
 
 
 Environment = Env
+_BASE_INFO = Scenario.info
 
 
 def _make_world(scenario: Scenario, batch_size: int, rng, device) -> World:

@@ -90,6 +90,8 @@ class FusedScenario(Scenario):
 
     # ---- launches -------------------------------------------------------------
     def alloc_outputs(self, world: World, obs_dim: int):
+        """Fresh (obs (A, Bp, O), rew (A, B), done (B,)); Bp pads B so that every
+        agent block starts 16-byte aligned (coalesced float4 stores)."""
         A, B = len(world.agents), world.batch_size
         bp = B
         while (bp * obs_dim) % 4:
@@ -99,31 +101,35 @@ class FusedScenario(Scenario):
         done = torch.empty(B, dtype=torch.bool, device=world.device)
         return obs, rew, done
 
-    def launch(self, world: World, mode: int, forces=None, raw_forces: bool = False, guard=None,
-               flip_rng: bool = True):
-        """One fused launch in `mode`; returns (obs (A, Bp, O), rew (A, B), done (B,))."""
+    def launch(self, world: World, mode: int, action_ptrs=None, raw_forces: bool = False,
+               guard=None, flip_rng: bool = True, stream: int | None = None):
+        """One fused launch in `mode`; returns (obs (A, Bp, O), rew (A, B), done (B,)).
+
+        action_ptrs: one device pointer per agent to a contiguous (B, 2) f32
+        block (the caller keeps the tensors alive until the launch is queued).
+        """
         world.ensure_device_rng()
         h = self.native_handle(world)
-        dev = world.device
-        st = N.stream_handle(dev)
+        st = stream if stream is not None else N.stream_handle(world.device)
         if (mode & N.DO_PHYSICS) and not self.physics_fused(world):
             from ..dynamics import run_world_step
 
-            run_world_step(world, forces, decode_mask=0 if raw_forces else (1 << 256) - 1, count=False)
+            run_world_step(world, action_ptrs, decode_mask=0 if raw_forces else (1 << 256) - 1,
+                           count=False, stream=st)
             mode &= ~N.DO_PHYSICS
         obs, rew, done = self.alloc_outputs(world, h.obs_dim)
-        io = N.SsStepIO()
-        ptrs = N.pointer_array(forces or [])
-        io.actions = ptrs
-        io.obs = N.ptr(obs)
+        io = h.io
+        if action_ptrs:
+            for i, p in enumerate(action_ptrs):
+                h.act_ptrs[i] = p
+        io.obs = obs.data_ptr()
         io.obs_agent_stride = obs.shape[1] * obs.shape[2]
-        io.rew = N.ptr(rew)
-        io.done = N.ptr(done)
+        io.rew = rew.data_ptr()
+        io.done = done.data_ptr()
         io.mode = mode
-        io.guard = N.ptr(guard)
+        io.guard = guard.data_ptr() if guard is not None else None
         io.raw_forces = int(raw_forces)
-        buf = world.buffers()
-        N.check(N.lib().ss_env_step(h.handle, ctypes.byref(buf), ctypes.byref(io), st))
+        N.check(N.lib().ss_env_step(h.handle, world.buffers_ref(), h.io_ref, st))
         if flip_rng and (mode & N.DO_POST) and self.advances_rng_per_step:
             world.rng.flip()
         return obs, rew, done
@@ -169,9 +175,8 @@ class FusedScenario(Scenario):
     def _reset(self, world: World, mask, mask_base=None, mask_total=None) -> None:
         world.ensure_device_rng()
         h = self.native_handle(world)
-        buf = world.buffers()
         m = None if mask is None else mask.to(world.device, torch.uint8).contiguous()
-        N.check(N.lib().ss_reset(h.handle, ctypes.byref(buf), N.ptr(m), N.ptr(mask_base),
+        N.check(N.lib().ss_reset(h.handle, world.buffers_ref(), N.ptr(m), N.ptr(mask_base),
                                  N.ptr(mask_total), N.stream_handle(world.device)))
         world.rng.flip()
 

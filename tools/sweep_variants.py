@@ -1,0 +1,62 @@
+"""Time the fused step kernel of each workload for several library variants.
+
+    python tools/sweep_variants.py LIB [LIB ...]
+
+Each LIB is loaded in a fresh subprocess (SS_LIB_PATH) and every workload
+is stepped with device-resident actions; prints the median per-launch time
+(CUDA events) and the implied HBM roofline fraction.
+"""
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+
+CHILD = r"""
+import json, sys
+sys.path.insert(0, %(root)r)
+import numpy as np, torch
+from bench import WORKLOADS, bytes_per_env_step, peaks
+from paper_2207_03530_b200 import Env, create_scenario
+out = {}
+for name in %(names)r:
+    scen, ov, B = WORKLOADS[name]
+    env = Env(create_scenario(scen, **ov), B, seed=0, device="cuda:0", validate=False)
+    A = len(env.agents); O = env.observations()[0].shape[1]
+    acts = [torch.rand((A, B, 2), device="cuda:0") * 2 - 1 for _ in range(4)]
+    for k in range(10): env.step(acts[k % 4])
+    torch.cuda.synchronize()
+    ts = []
+    for k in range(30):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(); env.step(acts[k % 4]); e.record()
+        ts.append((s, e))
+    torch.cuda.synchronize()
+    ms = float(np.median([s.elapsed_time(e) for s, e in ts]))
+    bpe = bytes_per_env_step(scen, A, len(env.world.entities) - A, O)
+    out[name] = {"ms": ms, "frac": bpe * B / (ms / 1e3) / 1e9 / peaks()["hbm_gbs"]}
+print("RESULT " + json.dumps(out))
+"""
+
+
+def main() -> None:
+    libs = sys.argv[1:]
+    names = os.environ.get("SWEEP_WORKLOADS", "simple_spread,transport,flocking,dispersion,discovery").split(",")
+    for lib in libs:
+        env = dict(os.environ, SS_LIB_PATH=str(Path(lib).resolve()))
+        code = CHILD.replace("%(root)r", repr(str(ROOT))).replace("%(names)r", repr(names))
+        res = subprocess.run([sys.executable, "-c", code],
+                             env=env, capture_output=True, text=True)
+        line = next((l for l in res.stdout.splitlines() if l.startswith("RESULT ")), None)
+        if line is None:
+            print(lib, "FAILED", res.stderr[-2000:])
+            continue
+        d = json.loads(line[7:])
+        print(Path(lib).name, " ".join(f"{k}={v['ms']*1e3:.1f}us({v['frac']*100:.0f}%)" for k, v in d.items()),
+              flush=True)
+
+
+if __name__ == "__main__":
+    main()
