@@ -87,6 +87,8 @@ typedef struct SsPairDesc {
   int32_t i, j;
   float d_min;            /* f32(min_contact_distance)      shapes.py:65     */
   float sign;             /* +1 if (i+j) even else -1       dynamics.py:169  */
+  float d2_act;           /* largest f32 x with fl(sqrt(x)) <= d_min: the pair is
+                             active iff x*x+y*y <= d2_act (no sqrt needed)     */
 } SsPairDesc;
 
 /* One reset action in scenario call order (common.py:11-34). */

@@ -38,7 +38,7 @@ class SsEntityDesc(ctypes.Structure):
 
 
 class SsPairDesc(ctypes.Structure):
-    _fields_ = [("i", c_i32), ("j", c_i32), ("d_min", c_f32), ("sign", c_f32)]
+    _fields_ = [("i", c_i32), ("j", c_i32), ("d_min", c_f32), ("sign", c_f32), ("d2_act", c_f32)]
 
 
 class SsResetOp(ctypes.Structure):

@@ -25,6 +25,7 @@ import numpy as np
 import torch
 
 from . import _native as N
+from ._numerics import sqrt_le_bound
 from .batching import DeviceRng, SeededRng, Vec2, as_f32, default_device, scalars
 from .errors import ContractViolation, UnsupportedShapePair
 from .shapes import Shape, Sphere, min_contact_distance, native_shape
@@ -478,7 +479,9 @@ class World:
         arr = (N.SsPairDesc * max(1, len(pairs)))()
         for n, (i, j) in enumerate(pairs):
             arr[n].i, arr[n].j = i, j
-            arr[n].d_min = np.float32(min_contact_distance(self.entities[i].shape, self.entities[j].shape))
+            dmin = np.float32(min_contact_distance(self.entities[i].shape, self.entities[j].shape))
+            arr[n].d_min = dmin
+            arr[n].d2_act = sqrt_le_bound(dmin)
             arr[n].sign = 1.0 if (i + j) % 2 == 0 else -1.0
         return arr, len(pairs)
 

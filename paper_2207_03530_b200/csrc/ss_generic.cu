@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(32) k_generic_physics(const GenericArgs a) {
     V2 oi, oj;
     if (!closest_points(pi, ri, si, pj, rj, sj, oi, oj)) { *a.status = 1; return; }
     float fx, fy;
-    if (!contact_force(oi.x, oi.y, oj.x, oj.y, pr.d_min, pr.sign, a.ph.ck, a.ph.k, fx, fy)) continue;
+    if (!contact_force(oi.x, oi.y, oj.x, oj.y, pr.d_min, pr.d2_act, pr.sign, a.ph.ck, a.ph.k, fx, fy)) continue;
     FX[pr.i * 32 + lane] = fadd(FX[pr.i * 32 + lane], fx);
     FY[pr.i * 32 + lane] = fadd(FY[pr.i * 32 + lane], fy);
     FX[pr.j * 32 + lane] = fsub(FX[pr.j * 32 + lane], fx);
@@ -142,13 +142,25 @@ int launch_generic(World& w, const SsBuffers* buf, const SsStepIO* io, const uin
 }
 
 // ---- function-level kernels -------------------------------------------------
+// largest float x >= 0 with fl(sqrt(x)) <= t (host; mirrors _numerics.py)
+float sqrt_le_bound(float t) {
+  if (!(t >= 0.0f)) return -1.0f;
+  if (isinf(t)) return t;
+  float x = t * t;
+  while (sqrtf(x) > t) x = nextafterf(x, 0.0f);
+  for (;;) {
+    const float nx = nextafterf(x, INFINITY);
+    if (sqrtf(nx) <= t) x = nx; else return x;
+  }
+}
+
 __global__ void k_collision_force(const float* pix, const float* piy, const float* pjx,
-                                  const float* pjy, float dmin, float sign, float ck, float k,
-                                  float* fx, float* fy, uint8_t* active, int64_t n) {
+                                  const float* pjy, float dmin, float d2_act, float sign, float ck,
+                                  float k, float* fx, float* fy, uint8_t* active, int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   float x, y;
-  active[i] = contact_force(pix[i], piy[i], pjx[i], pjy[i], dmin, sign, ck, k, x, y) ? 1 : 0;
+  active[i] = contact_force(pix[i], piy[i], pjx[i], pjy[i], dmin, d2_act, sign, ck, k, x, y) ? 1 : 0;
   fx[i] = x;
   fy[i] = y;
 }
@@ -203,8 +215,8 @@ int launch_collision_force(const float* pix, const float* piy, const float* pjx,
                            float dmin, float sign, float ck, float k, float* fx, float* fy,
                            uint8_t* active, int64_t n, cudaStream_t st) {
   if (n <= 0) return SS_OK;
-  k_collision_force<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pix, piy, pjx, pjy, dmin, sign,
-                                                                 ck, k, fx, fy, active, n);
+  k_collision_force<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+      pix, piy, pjx, pjy, dmin, sqrt_le_bound(dmin), sign, ck, k, fx, fy, active, n);
   return cuda_status(cudaGetLastError(), "collision_force launch");
 }
 

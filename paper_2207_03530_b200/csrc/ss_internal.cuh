@@ -86,13 +86,17 @@ inline PhysK make_phys(const World& w) {
 SS_DEV float clip_sym(float x, float u) { return fminf(fmaxf(x, -u), u); }
 
 // collision_force (dynamics.py:36-66) for one env: force on i (j gets -f).
-// Returns the active flag; inactive pairs contribute nothing.
-SS_DEV bool contact_force(float pix, float piy, float pjx, float pjy, float dmin, float sign,
-                          float ck, float k, float& fx, float& fy) {
+// Returns the active flag; inactive pairs contribute nothing.  The activity
+// test `norm <= d_min` is decided on the squared distance against
+// d2_act = max{x : fl(sqrt(x)) <= d_min} (host-computed, _numerics.py), which
+// is exactly equivalent; the square root is only taken for active pairs.
+SS_DEV bool contact_force(float pix, float piy, float pjx, float pjy, float dmin, float d2_act,
+                          float sign, float ck, float k, float& fx, float& fy) {
   const float x = fsub(pix, pjx);
   const float y = fsub(piy, pjy);
-  const float d = norm2(x, y);
-  if (!(d <= dmin)) { fx = 0.0f; fy = 0.0f; return false; }
+  const float d2 = fadd(fmul(x, x), fmul(y, y));
+  if (!(d2 <= d2_act)) { fx = 0.0f; fy = 0.0f; return false; }
+  const float d = fsqrt(d2);
   float dx, dy;
   if (d < 1e-8f) { dx = sign; dy = 0.0f; }            // DEGENERATE_DIST, dynamics.py:23
   else { dx = fdiv(x, d); dy = fdiv(y, d); }

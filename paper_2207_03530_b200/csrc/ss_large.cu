@@ -1,16 +1,24 @@
 // ss_large.cu — fused Env.step for the many-agent built-ins (dispersion,
 // discovery): one warp per environment, 8 environments per CTA.  Lane l owns
-// agents l, l+32, ... (T per lane); the env's positions/velocities are staged
-// in shared memory so every lane can read every partner (broadcast loads).
+// agents l, l+32, ... (T per lane); the env's positions/velocities and its
+// landmarks are staged in shared memory so every lane reads every partner
+// with broadcast loads.
 //
 // Pair forces (discovery, all agent pairs): each lane accumulates the force
 // on ITS agent k over partners j in the reference's pair-list order
 // (dynamics.py:163-180): pairs (j, k) with j < k subtract f(j,k), then pairs
 // (k, j) with j > k add f(k,j) — every f evaluated with the reference's own
-// operand order, so the sum is bit-identical without any cross-lane
-// communication.  Observation rows (34.8 KB / 50 KB per env, >90% of the
-// step's HBM bytes) are built in shared memory and streamed out with
-// coalesced 16-byte stores.
+// operand order, so the sum is bit-identical without cross-lane traffic.
+// Range decisions (contact, coverage, eating) compare squared distances with
+// host-computed exact bounds (_numerics.py); square roots are only taken for
+// values the reference actually produces (active contacts, reward terms).
+//
+// Observations are >90% of these steps' HBM bytes.  Every row of agent k is
+// "template minus own position": the template (landmarks, all agents,
+// eaten flags) is built once per env in shared memory, and the A rows are
+// produced as one flattened run of 16-byte chunks — lane l writes chunks
+// l, l+32, ... across all rows — straight from registers with streaming
+// stores, so each warp store instruction covers 512 contiguous bytes.
 #include "ss_internal.cuh"
 
 namespace ss {
@@ -31,10 +39,11 @@ struct LargeArgs {
   int mode;
   int raw_forces;
   const int* guard;
-  int NA, NL, O;    // agents, landmarks (points / food), obs width
+  int NA, NL, O;     // agents, landmarks (points / food), obs width
   int W;             // flag words
   float dmin;        // discovery: f32(r_a + r_b)
-  float thr;         // discovery: f32(cover_dist) | dispersion: f32(eat_dist)
+  float d2_act;      // discovery: squared-distance bound of dmin
+  float thr2;        // discovery cover_dist / dispersion eat_dist, squared bound
   int quorum;
   double lo_x, lo_y, range_x, range_y;   // discovery relocation box
 };
@@ -45,53 +54,58 @@ SS_DEV float warp_min(float v) {
   return v;
 }
 
-// Stream a staged row (16-byte aligned smem, O floats) to global memory.
-SS_DEV void flush_row(float* __restrict__ dst, const float* __restrict__ row, int O) {
-  const int lane = threadIdx.x & 31;
-  __syncwarp();
-  if ((reinterpret_cast<uintptr_t>(dst) & 15u) != 0) {
-    for (int i = lane; i < O; i += 32) __stcs(dst + i, row[i]);
-    __syncwarp();
-    return;
-  }
-  const int n4 = O >> 2;
-  float4* d4 = reinterpret_cast<float4*>(dst);
-  const float4* s4 = reinterpret_cast<const float4*>(row);
-  for (int i = lane; i < n4; i += 32) __stcs(d4 + i, s4[i]);
-  for (int i = (n4 << 2) + lane; i < O; i += 32) __stcs(dst + i, row[i]);
-  __syncwarp();
-}
-
+// Per-warp shared memory.  tmpl is the observation template:
+//   discovery : float2 slots [2 pad][NL landmarks][NA agents]  (lm, pos alias it)
+//   dispersion: floats [4 pad][NL x (fx, fy, eaten)]
 struct WarpSmem {
   float2* pos;     // [NA]
   float2* vel;     // [NA]
   float2* lm;      // [NL] landmark positions
+  float* tmpl;     // template (16-byte aligned)
   float* tmp;      // [2*NL] per-landmark scratch
   uint32_t* bits;  // [4] landmark flag words
-  float* row;      // [O] (16-byte aligned)
 };
 
-SS_DEV WarpSmem carve(float* base, int NA, int NL, int O) {
-  // per-warp footprint, rounded to 16 bytes
+__host__ __device__ inline int round4(int n) { return (n + 3) & ~3; }
+
+// First region: discovery's float2 template [2 + NL + NA], or dispersion's
+// float template [4 + 3 NL] followed by its agent positions [NA] (float2).
+__host__ __device__ inline int tmpl_floats(int NA, int NL) {
+  const int disc = 2 * (2 + NL + NA);
+  const int disp = round4(4 + 3 * NL) + 2 * NA;
+  return round4(disc > disp ? disc : disp);
+}
+
+__host__ __device__ inline int warp_floats(int NA, int NL) {
+  return tmpl_floats(NA, NL) + round4(2 * NA) /*vel*/ + round4(2 * NL) /*lm*/ + round4(2 * NL) /*tmp*/ + 4;
+}
+
+SS_DEV WarpSmem carve(float* base, int NA, int NL, bool discovery) {
   WarpSmem w;
-  w.pos = reinterpret_cast<float2*>(base);
-  w.vel = w.pos + NA;
-  w.lm = w.vel + NA;
-  w.tmp = reinterpret_cast<float*>(w.lm + NL);
-  w.bits = reinterpret_cast<uint32_t*>(w.tmp + 2 * NL);
-  const int used = 4 * NA + 2 * NL + 2 * NL + 4;
-  w.row = base + ((used + 3) & ~3);
+  const int t = tmpl_floats(NA, NL);
+  w.tmpl = base;
+  float* p = base + t;
+  w.vel = reinterpret_cast<float2*>(p);
+  p += round4(2 * NA);
+  if (discovery) {
+    float2* t2 = reinterpret_cast<float2*>(base);
+    w.lm = t2 + 2;
+    w.pos = t2 + 2 + NL;
+  } else {
+    w.lm = reinterpret_cast<float2*>(p);
+    w.pos = reinterpret_cast<float2*>(base + round4(4 + 3 * NL));
+  }
+  p += round4(2 * NL);
+  w.tmp = p;
+  p += round4(2 * NL);
+  w.bits = reinterpret_cast<uint32_t*>(p);
   return w;
 }
 
-__host__ __device__ inline int warp_floats(int NA, int NL, int O) {
-  const int used = 4 * NA + 2 * NL + 2 * NL + 4;
-  return ((used + 3) & ~3) + ((O + 3) & ~3);
-}
-
-// Load own agents, decode + integrate (no pair forces unless PAIRS).
+// Load own agents, decode + integrate (pair forces only when PAIRS).
+// Leaves post-step positions in sm.pos (or `posbuf`) and velocities in sm.vel.
 template <int T, bool PAIRS>
-SS_DEV void agents_physics(const LargeArgs& a, const WarpSmem& sm, int64_t e, float (&px)[T],
+SS_DEV void agents_physics(const LargeArgs& a, float2* pos, float2* vel, int64_t e, float (&px)[T],
                            float (&py)[T], float (&vx)[T], float (&vy)[T]) {
   const int lane = threadIdx.x & 31;
   const int64_t B = a.s.B;
@@ -101,73 +115,85 @@ SS_DEV void agents_physics(const LargeArgs& a, const WarpSmem& sm, int64_t e, fl
     if (k < a.NA) {
       const float4 q = a.s.dyn[k * B + e];
       px[t] = q.x; py[t] = q.y; vx[t] = q.z; vy[t] = q.w;
-      sm.pos[k] = make_float2(q.x, q.y);
+      pos[k] = make_float2(q.x, q.y);
     }
   }
   __syncwarp();
-  if (!(a.mode & SS_DO_PHYSICS)) {
+  if (a.mode & SS_DO_PHYSICS) {
+    float fx[T], fy[T];
 #pragma unroll
     for (int t = 0; t < T; ++t) {
       const int k = lane + 32 * t;
-      if (k < a.NA) sm.vel[k] = make_float2(vx[t], vy[t]);
+      fx[t] = 0.0f; fy[t] = 0.0f;
+      if (k < a.NA) {
+        const SsEntityDesc& d = a.ents[k];
+        const float2 u = a.act[k][e];
+        fx[t] = a.raw_forces ? u.x : fmul(clip_sym(u.x, d.u_range), d.u_mult);
+        fy[t] = a.raw_forces ? u.y : fmul(clip_sym(u.y, d.u_range), d.u_mult);
+        if (a.ph.has_gravity) { fx[t] = fadd(fx[t], d.grav_x); fy[t] = fadd(fy[t], d.grav_y); }
+      }
     }
-    __syncwarp();
-    return;
-  }
-  float fx[T], fy[T];
+    if (PAIRS) {
+      for (int j = 0; j < a.NA; ++j) {
+        const float2 pj = pos[j];
 #pragma unroll
-  for (int t = 0; t < T; ++t) {
-    const int k = lane + 32 * t;
-    fx[t] = 0.0f; fy[t] = 0.0f;
-    if (k < a.NA) {
-      const SsEntityDesc& d = a.ents[k];
-      const float2 u = a.act[k][e];
-      fx[t] = a.raw_forces ? u.x : fmul(clip_sym(u.x, d.u_range), d.u_mult);
-      fy[t] = a.raw_forces ? u.y : fmul(clip_sym(u.y, d.u_range), d.u_mult);
-      if (a.ph.has_gravity) { fx[t] = fadd(fx[t], d.grav_x); fy[t] = fadd(fy[t], d.grav_y); }
-    }
-  }
-  if (PAIRS) {
-    for (int j = 0; j < a.NA; ++j) {
-      const float2 pj = sm.pos[j];
-#pragma unroll
-      for (int t = 0; t < T; ++t) {
-        const int k = lane + 32 * t;
-        if (k >= a.NA || j == k) continue;
-        const float sign = ((j + k) & 1) ? -1.0f : 1.0f;
-        float cx, cy;
-        if (j < k) {
-          if (contact_force(pj.x, pj.y, px[t], py[t], a.dmin, sign, a.ph.ck, a.ph.k, cx, cy)) {
-            fx[t] = fsub(fx[t], cx); fy[t] = fsub(fy[t], cy);
-          }
-        } else {
-          if (contact_force(px[t], py[t], pj.x, pj.y, a.dmin, sign, a.ph.ck, a.ph.k, cx, cy)) {
-            fx[t] = fadd(fx[t], cx); fy[t] = fadd(fy[t], cy);
+        for (int t = 0; t < T; ++t) {
+          const int k = lane + 32 * t;
+          if (k >= a.NA || j == k) continue;
+          const float sign = ((j + k) & 1) ? -1.0f : 1.0f;
+          float cx, cy;
+          if (j < k) {
+            if (contact_force(pj.x, pj.y, px[t], py[t], a.dmin, a.d2_act, sign, a.ph.ck, a.ph.k, cx, cy)) {
+              fx[t] = fsub(fx[t], cx); fy[t] = fsub(fy[t], cy);
+            }
+          } else {
+            if (contact_force(px[t], py[t], pj.x, pj.y, a.dmin, a.d2_act, sign, a.ph.ck, a.ph.k, cx, cy)) {
+              fx[t] = fadd(fx[t], cx); fy[t] = fadd(fy[t], cy);
+            }
           }
         }
       }
     }
+    __syncwarp();   // everyone done reading the pre-step positions
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const int k = lane + 32 * t;
+      if (k < a.NA) {
+        const SsEntityDesc& d = a.ents[k];
+        integrate_lin(px[t], py[t], vx[t], vy[t], fx[t], fy[t], a.ph.keep, d.inv_m_dt, a.ph.dt,
+                      d.max_speed);
+        a.s.dyn[k * B + e] = make_float4(px[t], py[t], vx[t], vy[t]);
+        pos[k] = make_float2(px[t], py[t]);
+      }
+    }
   }
-  __syncwarp();   // everyone done reading the pre-step positions
 #pragma unroll
   for (int t = 0; t < T; ++t) {
     const int k = lane + 32 * t;
-    if (k < a.NA) {
-      const SsEntityDesc& d = a.ents[k];
-      integrate_lin(px[t], py[t], vx[t], vy[t], fx[t], fy[t], a.ph.keep, d.inv_m_dt, a.ph.dt,
-                    d.max_speed);
-      a.s.dyn[k * B + e] = make_float4(px[t], py[t], vx[t], vy[t]);
-      sm.pos[k] = make_float2(px[t], py[t]);
-      sm.vel[k] = make_float2(vx[t], vy[t]);
-    }
+    if (k < a.NA) vel[k] = make_float2(vx[t], vy[t]);
   }
   __syncwarp();
 }
 
+// Walk the flattened (row, chunk) space: lane handles idx = lane + 32*u.
+struct ChunkWalk {
+  int r, c;
+  float* rowp;
+  SS_DEV ChunkWalk(int start, int nch, float* base, int64_t stride) {
+    r = start / nch;
+    c = start - r * nch;
+    rowp = base + r * stride;
+  }
+  SS_DEV void advance(int nch, int64_t stride) {
+    c += 32;
+    while (c >= nch) { c -= nch; ++r; rowp += stride; }
+  }
+};
+
 // ---------------------------------------------------------------------------
 // discovery (scenarios/discovery.py)
 // ---------------------------------------------------------------------------
-template <int T>
+template <int T, int VEC>
 __global__ void __launch_bounds__(32 * kLargeWarps) k_discovery(const LargeArgs a) {
   extern __shared__ __align__(16) float smem[];
   if (a.guard && *a.guard) return;
@@ -179,27 +205,25 @@ __global__ void __launch_bounds__(32 * kLargeWarps) k_discovery(const LargeArgs 
     philox_advance(a.s.rng_in, 2ull * (uint64_t)a.NL * Bg, a.s.rng_out);
   }
   if (e >= B) return;
-  const WarpSmem sm = carve(smem + wid * warp_floats(a.NA, a.NL, a.O), a.NA, a.NL, a.O);
+  const WarpSmem sm = carve(smem + wid * warp_floats(a.NA, a.NL), a.NA, a.NL, true);
   for (int i = lane; i < a.NL; i += 32) sm.lm[i] = a.s.stat[i * B + e];
   float px[T], py[T], vx[T], vy[T];
-  agents_physics<T, true>(a, sm, e, px, py, vx, vy);
+  agents_physics<T, true>(a, sm.pos, sm.vel, e, px, py, vx, vy);
 
   int64_t steps = 0;
   if (a.mode & (SS_DO_COUNT | SS_DO_DONE)) {
     steps = a.s.step_count[e];
-    if ((a.mode & SS_DO_COUNT)) { steps += 1; if (lane == 0) a.s.step_count[e] = steps; }
+    if (a.mode & SS_DO_COUNT) { steps += 1; if (lane == 0) a.s.step_count[e] = steps; }
   }
   // post_step (discovery.py:57-71): coverage, then a relocation draw for
   // every env and every point regardless of coverage.
   if (a.mode & SS_DO_POST) {
     const uint64_t eg = (uint64_t)(a.s.env_offset + e);
-    // relocation draws for all points, one lane per (point, axis)
-    for (int l = lane; l < 2 * a.NL; l += 32) {
+    for (int l = lane; l < 2 * a.NL; l += 32) {   // one lane per (point, axis) draw
       const int i = l >> 1, axis = l & 1;
       sm.tmp[l] = uniform_f32(philox_draw(a.s.rng_in, (uint64_t)(2 * i + axis) * Bg + eg),
                               axis ? a.lo_y : a.lo_x, axis ? a.range_y : a.range_x);
     }
-    __syncwarp();
     for (int w = 0; w < a.W; ++w) {
       uint32_t bits = 0u;
       for (int b = 0; b < 32; ++b) {
@@ -211,13 +235,12 @@ __global__ void __launch_bounds__(32 * kLargeWarps) k_discovery(const LargeArgs 
         for (int t = 0; t < T; ++t) {
           const int k = lane + 32 * t;
           bool in = false;
-          if (k < a.NA) in = norm2(fsub(px[t], pt.x), fsub(py[t], pt.y)) <= a.thr;
+          if (k < a.NA) in = sqnorm(fsub(px[t], pt.x), fsub(py[t], pt.y)) <= a.thr2;
           c += __popc(__ballot_sync(0xffffffffu, in));
         }
         if (c >= a.quorum) bits |= 1u << b;
       }
-      if (lane == 0) a.s.flags[w * B + e] = bits;
-      sm.bits[w] = bits;
+      if (lane == 0) { a.s.flags[w * B + e] = bits; sm.bits[w] = bits; }
     }
     __syncwarp();
     for (int i = lane; i < a.NL; i += 32) {
@@ -231,7 +254,8 @@ __global__ void __launch_bounds__(32 * kLargeWarps) k_discovery(const LargeArgs 
   }
   if (a.mode & SS_DO_REWARD) {
     // score = #covered (float64); crowding = sum over points of the
-    // quorum-th nearest agent distance (np.partition), float64 accumulator.
+    // quorum-th nearest agent distance (np.partition), float64 accumulator;
+    // the order statistic is taken on squared distances, then one sqrt.
     int score = 0;
     for (int w = 0; w < a.W; ++w) score += __popc((a.mode & SS_DO_POST) ? sm.bits[w] : a.s.flags[w * B + e]);
     double crowding = 0.0;
@@ -241,7 +265,7 @@ __global__ void __launch_bounds__(32 * kLargeWarps) k_discovery(const LargeArgs 
 #pragma unroll
       for (int t = 0; t < T; ++t) {
         const int k = lane + 32 * t;
-        v[t] = (k < a.NA) ? norm2(fsub(px[t], pt.x), fsub(py[t], pt.y)) : __int_as_float(0x7f800000);
+        v[t] = (k < a.NA) ? sqnorm(fsub(px[t], pt.x), fsub(py[t], pt.y)) : __int_as_float(0x7f800000);
       }
       float kth = 0.0f;
       for (int r = 0; r < a.quorum; ++r) {
@@ -251,14 +275,14 @@ __global__ void __launch_bounds__(32 * kLargeWarps) k_discovery(const LargeArgs 
         kth = warp_min(mine);
         const unsigned has = __ballot_sync(0xffffffffu, mine == kth);
         if (lane == __ffs(has) - 1) {
-          bool done_rm = false;
+          bool removed = false;
 #pragma unroll
           for (int t = 0; t < T; ++t) {
-            if (!done_rm && v[t] == kth) { v[t] = __int_as_float(0x7f800000); done_rm = true; }
+            if (!removed && v[t] == kth) { v[t] = __int_as_float(0x7f800000); removed = true; }
           }
         }
       }
-      crowding = dadd_rn(crowding, (double)kth);
+      crowding = dadd_rn(crowding, (double)fsqrt(kth));
     }
     const float r = (float)dsub_rn((double)score, dmul_rn(0.05, crowding));
 #pragma unroll
@@ -270,24 +294,35 @@ __global__ void __launch_bounds__(32 * kLargeWarps) k_discovery(const LargeArgs 
   if ((a.mode & SS_DO_DONE) && lane == 0) a.done[e] = (uint8_t)(steps >= a.ph.max_steps);
   if (a.mode & SS_DO_OBS) {
     // row(k) = [x, y, vx, vy, (point_i - a_k)_i, (a_o - a_k)_{o != k}]
+    // template slots: tmpl2[2 + i] = point_i, tmpl2[2 + NL + o] = a_o
+    const float2* t2 = reinterpret_cast<const float2*>(sm.tmpl);
+    const int first_agent_slot = 2 + a.NL;
     const int slots = a.O >> 1;
-    float2* row2 = reinterpret_cast<float2*>(sm.row);
-    for (int k = 0; k < a.NA; ++k) {
-      const float2 pk = sm.pos[k];
-      for (int q = lane; q < slots; q += 32) {
+    const int nch = slots / (VEC / 2);          // chunks per row
+    const int total = a.NA * nch;
+    ChunkWalk w(lane, nch, a.obs + e * a.O, a.obs_stride);
+    for (int idx = lane; idx < total; idx += 32) {
+      const float2 pk = sm.pos[w.r];
+      float2 out[VEC / 2];
+#pragma unroll
+      for (int h = 0; h < VEC / 2; ++h) {
+        const int s = w.c * (VEC / 2) + h;
         float2 v;
-        if (q == 0) v = pk;
-        else if (q == 1) v = sm.vel[k];
-        else if (q < 2 + a.NL) { const float2 p = sm.lm[q - 2]; v = make_float2(fsub(p.x, pk.x), fsub(p.y, pk.y)); }
+        if (s == 0) v = pk;
+        else if (s == 1) v = sm.vel[w.r];
         else {
-          int o = q - 2 - a.NL;
-          o += (o >= k);
-          const float2 p = sm.pos[o];
-          v = make_float2(fsub(p.x, pk.x), fsub(p.y, pk.y));
+          const int src = (s >= first_agent_slot && s - first_agent_slot >= w.r) ? s + 1 : s;
+          const float2 q = t2[src];
+          v = make_float2(fsub(q.x, pk.x), fsub(q.y, pk.y));
         }
-        row2[q] = v;
+        out[h] = v;
       }
-      flush_row(a.obs + k * a.obs_stride + e * a.O, sm.row, a.O);
+      if (VEC == 4) {
+        __stcs(reinterpret_cast<float4*>(w.rowp) + w.c, make_float4(out[0].x, out[0].y, out[VEC / 2 - 1].x, out[VEC / 2 - 1].y));
+      } else {
+        __stcs(reinterpret_cast<float2*>(w.rowp) + w.c, out[0]);
+      }
+      w.advance(nch, a.obs_stride);
     }
   }
 }
@@ -295,7 +330,7 @@ __global__ void __launch_bounds__(32 * kLargeWarps) k_discovery(const LargeArgs 
 // ---------------------------------------------------------------------------
 // dispersion (scenarios/dispersion.py): agents non-collidable (no pairs).
 // ---------------------------------------------------------------------------
-template <int T>
+template <int T, int VEC>
 __global__ void __launch_bounds__(32 * kLargeWarps) k_dispersion(const LargeArgs a) {
   extern __shared__ __align__(16) float smem[];
   if (a.guard && *a.guard) return;
@@ -303,44 +338,44 @@ __global__ void __launch_bounds__(32 * kLargeWarps) k_dispersion(const LargeArgs
   const int64_t B = a.s.B;
   const int64_t e = (int64_t)blockIdx.x * kLargeWarps + wid;
   if (e >= B) return;
-  const WarpSmem sm = carve(smem + wid * warp_floats(a.NA, a.NL, a.O), a.NA, a.NL, a.O);
+  const WarpSmem sm = carve(smem + wid * warp_floats(a.NA, a.NL), a.NA, a.NL, false);
   for (int i = lane; i < a.NL; i += 32) sm.lm[i] = a.s.stat[i * B + e];
   float px[T], py[T], vx[T], vy[T];
-  agents_physics<T, false>(a, sm, e, px, py, vx, vy);
+  float2* apos = sm.pos;
+  agents_physics<T, false>(a, apos, sm.vel, e, px, py, vx, vy);
 
   int64_t steps = 0;
   if (a.mode & (SS_DO_COUNT | SS_DO_DONE)) {
     steps = a.s.step_count[e];
-    if ((a.mode & SS_DO_COUNT)) { steps += 1; if (lane == 0) a.s.step_count[e] = steps; }
+    if (a.mode & SS_DO_COUNT) { steps += 1; if (lane == 0) a.s.step_count[e] = steps; }
   }
-  // nearest-agent distance per food item: serves both post_step's "reached"
-  // (any d <= eat_dist  <=>  min d <= eat_dist) and reward's hunger term.
+  // nearest-agent squared distance per food item: serves post_step's
+  // "reached" (any d <= eat_dist  <=>  min d2 <= bound) and the hunger term
+  // (sqrt of the min).
   if (a.mode & (SS_DO_POST | SS_DO_REWARD)) {
     for (int i = lane; i < a.NL; i += 32) {
       const float2 f = sm.lm[i];
       float best = __int_as_float(0x7f800000);
       for (int j = 0; j < a.NA; ++j) {
-        const float2 p = sm.pos[j];
-        best = fminf(best, norm2(fsub(p.x, f.x), fsub(p.y, f.y)));
+        const float2 p = apos[j];
+        best = fminf(best, sqnorm(fsub(p.x, f.x), fsub(p.y, f.y)));
       }
       sm.tmp[i] = best;
     }
-    __syncwarp();
   }
-  uint32_t* eaten = sm.bits;
-  if (lane < a.W) eaten[lane] = a.s.flags[lane * B + e];
+  if (lane < a.W) sm.bits[lane] = a.s.flags[lane * B + e];
   __syncwarp();
   float fresh = 0.0f;
   if (a.mode & SS_DO_POST) {   // dispersion.py:56-66
     int newly = 0;
     for (int w = 0; w < a.W; ++w) {
       const int i = w * 32 + lane;
-      const bool reached = (i < a.NL) && (sm.tmp[i] <= a.thr);
+      const bool reached = (i < a.NL) && (sm.tmp[i] <= a.thr2);
       const uint32_t r = __ballot_sync(0xffffffffu, reached);
-      const uint32_t old = eaten[w];
+      const uint32_t old = sm.bits[w];
       newly += __popc(r & ~old);
       __syncwarp();
-      if (lane == 0) { eaten[w] = old | r; a.s.flags[w * B + e] = old | r; }
+      if (lane == 0) { sm.bits[w] = old | r; a.s.flags[w * B + e] = old | r; }
       __syncwarp();
     }
     fresh = (float)newly;
@@ -348,13 +383,13 @@ __global__ void __launch_bounds__(32 * kLargeWarps) k_dispersion(const LargeArgs
   } else if (a.mode & SS_DO_REWARD) {
     fresh = a.s.aux[e];
   }
-  if (a.mode & SS_DO_REWARD) {   // dispersion.py:68-76, float64 hunger
+  if (a.mode & SS_DO_REWARD) {   // dispersion.py:68-76, float64 hunger in item order
     float r = 0.0f;
     if (lane == 0) {
       double hunger = 0.0;
       for (int i = 0; i < a.NL; ++i) {
-        const bool ate = (eaten[i >> 5] >> (i & 31)) & 1u;
-        hunger = dadd_rn(hunger, ate ? 0.0 : (double)sm.tmp[i]);
+        const bool ate = (sm.bits[i >> 5] >> (i & 31)) & 1u;
+        hunger = dadd_rn(hunger, ate ? 0.0 : (double)fsqrt(sm.tmp[i]));
       }
       r = (float)dsub_rn((double)fresh, dmul_rn(0.05, hunger));
     }
@@ -367,24 +402,59 @@ __global__ void __launch_bounds__(32 * kLargeWarps) k_dispersion(const LargeArgs
   }
   if ((a.mode & SS_DO_DONE) && lane == 0) {
     bool all = true;
-    for (int i = 0; i < a.NL; ++i) all &= (bool)((eaten[i >> 5] >> (i & 31)) & 1u);
+    for (int w = 0; w < a.W; ++w) {
+      const int n = min(32, a.NL - 32 * w);
+      const uint32_t full = n == 32 ? 0xffffffffu : ((1u << n) - 1u);
+      all &= (sm.bits[w] & full) == full;
+    }
     a.done[e] = (uint8_t)(all | (steps >= a.ph.max_steps));
   }
   if (a.mode & SS_DO_OBS) {
-    // row(k) = [x, y, vx, vy, (food_i - a_k, eaten_i)_i]
-    for (int k = 0; k < a.NA; ++k) {
-      const float2 pk = sm.pos[k];
-      if (lane == 0) {
-        const float2 vk = sm.vel[k];
-        sm.row[0] = pk.x; sm.row[1] = pk.y; sm.row[2] = vk.x; sm.row[3] = vk.y;
+    // row(k) = [x, y, vx, vy, (food_i - a_k, eaten_i)_i]; template
+    // tmpl[4 + 3i .. 6 + 3i] = (food_i.x, food_i.y, eaten_i)
+    for (int i = lane; i < a.NL; i += 32) {
+      const float2 f = sm.lm[i];
+      sm.tmpl[4 + 3 * i] = f.x;
+      sm.tmpl[5 + 3 * i] = f.y;
+      sm.tmpl[6 + 3 * i] = ((sm.bits[i >> 5] >> (i & 31)) & 1u) ? 1.0f : 0.0f;
+    }
+    __syncwarp();
+    const int nch = a.O / VEC;
+    const int total = a.NA * nch;
+    ChunkWalk w(lane, nch, a.obs + e * a.O, a.obs_stride);
+    for (int idx = lane; idx < total; idx += 32) {
+      const float2 pk = apos[w.r];
+      if (VEC == 4) {
+        float4 v;
+        if (w.c == 0) {
+          const float2 vk = sm.vel[w.r];
+          v = make_float4(pk.x, pk.y, vk.x, vk.y);
+        } else {
+          // chunk c covers template floats 4c..4c+3; element 4c+u belongs to
+          // item field (c - 1 + u) % 3: 0 -> x (minus own x), 1 -> y, 2 -> flag.
+          // Subtracting +0 leaves the flag bitwise unchanged.
+          const int m = (w.c - 1) % 3;
+          const float4 t = reinterpret_cast<const float4*>(sm.tmpl)[w.c];
+          const float s0 = m == 0 ? pk.x : (m == 1 ? pk.y : 0.0f);
+          const float s1 = m == 0 ? pk.y : (m == 1 ? 0.0f : pk.x);
+          const float s2 = m == 0 ? 0.0f : (m == 1 ? pk.x : pk.y);
+          v = make_float4(fsub(t.x, s0), fsub(t.y, s1), fsub(t.z, s2), fsub(t.w, s0));
+        }
+        __stcs(reinterpret_cast<float4*>(w.rowp) + w.c, v);
+      } else {
+        const int j = w.c;
+        float x;
+        if (j < 4) {
+          const float2 vk = sm.vel[w.r];
+          x = j == 0 ? pk.x : (j == 1 ? pk.y : (j == 2 ? vk.x : vk.y));
+        } else {
+          const int t = (j - 4) % 3;
+          const float tv = sm.tmpl[j];
+          x = t == 0 ? fsub(tv, pk.x) : (t == 1 ? fsub(tv, pk.y) : tv);
+        }
+        __stcs(w.rowp + j, x);
       }
-      for (int i = lane; i < a.NL; i += 32) {
-        const float2 f = sm.lm[i];
-        sm.row[4 + 3 * i] = fsub(f.x, pk.x);
-        sm.row[5 + 3 * i] = fsub(f.y, pk.y);
-        sm.row[6 + 3 * i] = ((eaten[i >> 5] >> (i & 31)) & 1u) ? 1.0f : 0.0f;
-      }
-      flush_row(a.obs + k * a.obs_stride + e * a.O, sm.row, a.O);
+      w.advance(nch, a.obs_stride);
     }
   }
 }
@@ -399,7 +469,7 @@ int launch_large(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_
   a.NL = w.d.n_stat;
   a.O = w.d.obs_dim;
   a.W = w.d.n_flag_words;
-  if (a.NA < 1 || a.NA > kLargeMaxAgents || a.NL > kLargeMaxLandmarks) {
+  if (a.NA < 1 || a.NA > kLargeMaxAgents || a.NL > kLargeMaxLandmarks || a.W > 4) {
     set_error("fused many-agent kernel supports up to 128 agents and 128 landmarks");
     return SS_ERR_UNSUPPORTED;
   }
@@ -414,13 +484,15 @@ int launch_large(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_
   a.raw_forces = io->raw_forces;
   a.guard = io->guard;
   a.dmin = w.d.sc[0];
-  a.thr = w.d.sc[1];
+  a.d2_act = w.d.sc[2];
+  a.thr2 = w.d.sc[3];
   a.quorum = w.d.si[0];
   a.lo_x = w.d.sd[0]; a.lo_y = w.d.sd[1]; a.range_x = w.d.sd[2]; a.range_y = w.d.sd[3];
   const int64_t B = w.d.batch;
   const unsigned grid = (unsigned)((B + kLargeWarps - 1) / kLargeWarps);
-  const size_t shmem = (size_t)kLargeWarps * warp_floats(a.NA, a.NL, a.O) * sizeof(float);
+  const size_t shmem = (size_t)kLargeWarps * warp_floats(a.NA, a.NL) * sizeof(float);
   const int T = a.NA <= 32 ? 1 : (a.NA <= 64 ? 2 : 4);
+  const bool v4 = (a.O % 4) == 0 && (a.obs_stride % 4) == 0;
 #define SS_LAUNCH(K)                                                                   \
   do {                                                                                 \
     if (shmem > 48 * 1024)                                                             \
@@ -428,13 +500,17 @@ int launch_large(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_
     K<<<grid, 32 * kLargeWarps, shmem, st>>>(a);                                       \
   } while (0)
   if (w.d.scenario == SS_SCN_DISCOVERY) {
-    if (T == 1) SS_LAUNCH(k_discovery<1>);
-    else if (T == 2) SS_LAUNCH(k_discovery<2>);
-    else SS_LAUNCH(k_discovery<4>);
+    if (v4) {
+      if (T == 1) SS_LAUNCH((k_discovery<1, 4>)); else if (T == 2) SS_LAUNCH((k_discovery<2, 4>)); else SS_LAUNCH((k_discovery<4, 4>));
+    } else {
+      if (T == 1) SS_LAUNCH((k_discovery<1, 2>)); else if (T == 2) SS_LAUNCH((k_discovery<2, 2>)); else SS_LAUNCH((k_discovery<4, 2>));
+    }
   } else {
-    if (T == 1) SS_LAUNCH(k_dispersion<1>);
-    else if (T == 2) SS_LAUNCH(k_dispersion<2>);
-    else SS_LAUNCH(k_dispersion<4>);
+    if (v4) {
+      if (T == 1) SS_LAUNCH((k_dispersion<1, 4>)); else if (T == 2) SS_LAUNCH((k_dispersion<2, 4>)); else SS_LAUNCH((k_dispersion<4, 4>));
+    } else {
+      if (T == 1) SS_LAUNCH((k_dispersion<1, 1>)); else if (T == 2) SS_LAUNCH((k_dispersion<2, 1>)); else SS_LAUNCH((k_dispersion<4, 1>));
+    }
   }
 #undef SS_LAUNCH
   return cuda_status(cudaGetLastError(), "fused many-agent step launch");

@@ -80,8 +80,10 @@ SS_HD double dsub_rn(double a, double b) { return a - b; }
 SS_HD double dfma_rn(double a, double b, double c) { return fma(a, b, c); }
 #endif
 
+// x*x + y*y with the reference's rounding (the radicand of Vec2.norm).
+SS_HD float sqnorm(float x, float y) { return fadd(fmul(x, x), fmul(y, y)); }
 // sqrt(x*x + y*y) exactly as Vec2.norm (batching.py:129-130): no hypot, no FMA.
-SS_HD float norm2(float x, float y) { return fsqrt(fadd(fmul(x, x), fmul(y, y))); }
+SS_HD float norm2(float x, float y) { return fsqrt(sqnorm(x, y)); }
 
 // ---- glibc 2.39 expf (sysdeps/ieee754/flt-32/e_expf.c, FMA ifunc build) ----
 // Table: asuint64(2^(i/32)) - (i << 47), generated from exact decimal powers.

@@ -20,7 +20,7 @@ constexpr int kFlockMaxRocks = 6;
 constexpr int kSmallThreads = 128;
 // minimum resident CTAs per SM requested from ptxas (register budget)
 #ifndef SS_SMALL_MINB
-#define SS_SMALL_MINB 1
+#define SS_SMALL_MINB 6   // 6 x 128 threads: <= 80 registers, best measured (tools/sweep_variants.py)
 #endif
 
 struct SmallArgs {
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_simple_spread(
       for (int j = i + 1; j < NA; ++j, ++p) {
         const SsPairDesc pr = a.pairs[p];
         float cx, cy;
-        if (contact_force(px[i], py[i], px[j], py[j], pr.d_min, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
+        if (contact_force(px[i], py[i], px[j], py[j], pr.d_min, pr.d2_act, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
           fx[i] = fadd(fx[i], cx); fy[i] = fadd(fy[i], cy);
           fx[j] = fsub(fx[j], cx); fy[j] = fsub(fy[j], cy);
         }
@@ -147,14 +147,16 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_simple_spread(
     if (a.mode & SS_DO_COUNT) { steps += 1; a.s.step_count[e] = steps; }
   }
   if (valid && (a.mode & SS_DO_REWARD)) {
-    const float thr = a.sc[0], pen = a.sc[1];
+    const float pen = a.sc[1], thr2 = a.sc[2];
+    // min over agents of the distance = sqrt of the min squared distance
+    // (sqrt is monotonic and correctly rounded), one sqrt per marker.
     double cover = 0.0;   // np.zeros(B) float64 accumulator, simple_spread.py:41
 #pragma unroll
     for (int m = 0; m < NA; ++m) {
-      float best = norm2(fsub(px[0], mx[m]), fsub(py[0], my[m]));
+      float best = sqnorm(fsub(px[0], mx[m]), fsub(py[0], my[m]));
 #pragma unroll
-      for (int i = 1; i < NA; ++i) best = fminf(best, norm2(fsub(px[i], mx[m]), fsub(py[i], my[m])));
-      cover = dadd_rn(cover, (double)best);
+      for (int i = 1; i < NA; ++i) best = fminf(best, sqnorm(fsub(px[i], mx[m]), fsub(py[i], my[m])));
+      cover = dadd_rn(cover, (double)fsqrt(best));
     }
 #pragma unroll
     for (int i = 0; i < NA; ++i) {
@@ -162,7 +164,7 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_simple_spread(
 #pragma unroll
       for (int o = 0; o < NA; ++o) {
         if (o == i) continue;
-        coll = fadd(coll, norm2(fsub(px[i], px[o]), fsub(py[i], py[o])) <= thr ? 1.0f : 0.0f);
+        coll = fadd(coll, sqnorm(fsub(px[i], px[o]), fsub(py[i], py[o])) <= thr2 ? 1.0f : 0.0f);
       }
       __stcs(a.rew + i * B + e, (float)dsub_rn(-cover, (double)fmul(pen, coll)));
     }
@@ -245,7 +247,7 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_transport(cons
       for (int j = i + 1; j < NA; ++j, ++p) {
         const SsPairDesc pr = a.pairs[p];
         float cx, cy;
-        if (contact_force(px[i], py[i], px[j], py[j], pr.d_min, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
+        if (contact_force(px[i], py[i], px[j], py[j], pr.d_min, pr.d2_act, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
           fx[i] = fadd(fx[i], cx); fy[i] = fadd(fy[i], cy);
           fx[j] = fsub(fx[j], cx); fy[j] = fsub(fy[j], cy);
         }
@@ -254,7 +256,7 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_transport(cons
         const SsPairDesc pr = a.pairs[p++];
         float qx, qy, cx, cy;
         closest_point_on_box(px[i], py[i], px[NA], py[NA], ca, sa, hx, hy, qx, qy);
-        if (contact_force(px[i], py[i], qx, qy, pr.d_min, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
+        if (contact_force(px[i], py[i], qx, qy, pr.d_min, pr.d2_act, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
           fx[i] = fadd(fx[i], cx); fy[i] = fadd(fy[i], cy);
           fx[NA] = fsub(fx[NA], cx); fy[NA] = fsub(fy[NA], cy);
         }
@@ -309,9 +311,43 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_transport(cons
 // sc[2] = f32(collision_penalty); si[4] = NO; sd[0], sd[1] = agent / rock
 // radius^2 as python doubles (sensors.py:47).
 // ---------------------------------------------------------------------------
+// Conservative float32 screen of one (ray, circle) pair.  It returns false
+// only when the exact float64 test (ray_circle, sensors.py:43-54) is certain
+// to yield no hit or a hit beyond max_range — i.e. when skipping the pair
+// cannot change min(best, max_range).  Every surviving pair is evaluated in
+// float64 exactly as the reference, so the lidar output stays bit-identical.
+// Margins (1e-4) dominate the float32 rounding of these few products by
+// more than two orders of magnitude for |origin - centre| up to ~1e2; pairs
+// farther than max_range are rejected by the first test before that.
+struct RayScreen {
+  float rr;       // r + 1e-4
+  float reach2;   // (max_range + r + 1e-4)^2
+  float r2;       // r^2 (float32)
+};
+
+SS_DEV bool ray_may_hit(float fx, float fy, float dx, float dy, const RayScreen& s) {
+  const float f2 = fx * fx + fy * fy;
+  if (!(f2 <= s.reach2)) return false;       // every hit lies beyond max_range
+  const float cr = fx * dy - fy * dx;
+  if (fabsf(cr) > s.rr) return false;        // line misses the circle
+  const float b = fx * dx + fy * dy;
+  if (b > 1e-4f && f2 - s.r2 > 1e-4f) return false;   // circle behind an outside origin
+  return true;
+}
+
 struct FlockLidarK {
   double r2_agent, r2_rock;
+  RayScreen agent, rock;
 };
+
+inline RayScreen make_screen(double r, double max_range) {
+  RayScreen s;
+  s.rr = (float)r + 1e-4f;
+  const float reach = (float)max_range + s.rr;
+  s.reach2 = reach * reach;
+  s.r2 = (float)(r * r);
+  return s;
+}
 
 template <int NA>
 __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_flocking(const SmallArgs a, const FlockLidarK lk) {
@@ -356,7 +392,7 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_flocking(const
       for (int j = i + 1; j < NA; ++j, ++p) {
         const SsPairDesc pr = a.pairs[p];
         float cx, cy;
-        if (contact_force(px[i], py[i], px[j], py[j], pr.d_min, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
+        if (contact_force(px[i], py[i], px[j], py[j], pr.d_min, pr.d2_act, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
           fx[i] = fadd(fx[i], cx); fy[i] = fadd(fy[i], cy);
           fx[j] = fsub(fx[j], cx); fy[j] = fsub(fy[j], cy);
         }
@@ -366,7 +402,7 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_flocking(const
         if (r < NO) {
           const SsPairDesc pr = a.pairs[p++];
           float cx, cy;
-          if (contact_force(px[i], py[i], rx[r], ry[r], pr.d_min, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
+          if (contact_force(px[i], py[i], rx[r], ry[r], pr.d_min, pr.d2_act, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
             fx[i] = fadd(fx[i], cx); fy[i] = fadd(fy[i], cy);
           }
         }
@@ -386,7 +422,7 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_flocking(const
     if (a.mode & SS_DO_COUNT) { steps += 1; a.s.step_count[e] = steps; }
   }
   if (valid && (a.mode & SS_DO_REWARD)) {
-    const float thr_aa = a.sc[0], thr_ar = a.sc[1], pen = a.sc[2];
+    const float pen = a.sc[2], thr2_aa = a.sc[3], thr2_ar = a.sc[4];
 #pragma unroll
     for (int i = 0; i < NA; ++i) {
       const float gap = norm2(fsub(px[i], bx), fsub(py[i], by));
@@ -394,11 +430,11 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_flocking(const
 #pragma unroll
       for (int o = 0; o < NA; ++o) {
         if (o == i) continue;
-        ca = fadd(ca, norm2(fsub(px[i], px[o]), fsub(py[i], py[o])) <= thr_aa ? 1.0f : 0.0f);
+        ca = fadd(ca, sqnorm(fsub(px[i], px[o]), fsub(py[i], py[o])) <= thr2_aa ? 1.0f : 0.0f);
       }
 #pragma unroll
       for (int r = 0; r < kFlockMaxRocks; ++r) {
-        if (r < NO) cr = fadd(cr, norm2(fsub(px[i], rx[r]), fsub(py[i], ry[r])) <= thr_ar ? 1.0f : 0.0f);
+        if (r < NO) cr = fadd(cr, sqnorm(fsub(px[i], rx[r]), fsub(py[i], ry[r])) <= thr2_ar ? 1.0f : 0.0f);
       }
       __stcs(a.rew + i * B + e, fsub(-gap, fmul(pen, fadd(ca, cr))));
     }
@@ -437,15 +473,18 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_flocking(const
                                       (double)rot_i);
               sincos(ang, &dy, &dx);
             }
+            const float dx32 = (float)dx, dy32 = (float)dy;
             double best = __longlong_as_double(0x7ff0000000000000LL);
 #pragma unroll
             for (int o = 0; o < NA; ++o) {
               if (o == i) continue;
-              best = fmin(best, ray_circle(ox, oy, dx, dy, (double)px[o], (double)py[o], lk.r2_agent));
+              if (ray_may_hit(px[i] - px[o], py[i] - py[o], dx32, dy32, lk.agent))
+                best = fmin(best, ray_circle(ox, oy, dx, dy, (double)px[o], (double)py[o], lk.r2_agent));
             }
 #pragma unroll
             for (int r = 0; r < kFlockMaxRocks; ++r) {
-              if (r < NO) best = fmin(best, ray_circle(ox, oy, dx, dy, (double)rx[r], (double)ry[r], lk.r2_rock));
+              if (r < NO && ray_may_hit(px[i] - rx[r], py[i] - ry[r], dx32, dy32, lk.rock))
+                best = fmin(best, ray_circle(ox, oy, dx, dy, (double)rx[r], (double)ry[r], lk.r2_rock));
             }
             row[c + m] = (float)fmin(best, a.lidar_range);
           }
@@ -509,6 +548,8 @@ int launch_small(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_
       FlockLidarK lk;
       lk.r2_agent = w.d.sd[0];
       lk.r2_rock = w.d.sd[1];
+      lk.agent = make_screen(w.d.sd[2], w.d.lidar_max_range);
+      lk.rock = make_screen(w.d.sd[3], w.d.lidar_max_range);
       a.n_rays = w.d.lidar_rays;
       a.lidar_range = w.d.lidar_max_range;
       a.attach_rot = w.d.lidar_attach_rotation;

@@ -341,6 +341,19 @@ class Env:
             infos = [sc.info(a, world) for a in self.agents]
         return StepResult(obs=obs_list, rewards=list(rew.unbind(0)), dones=done, infos=infos)
 
+    def _capture_step(self, ptrs, keepalive) -> StepResult:
+        """One fused step without validation or host syncs (graph capture)."""
+        saved = self.validate
+        self.validate = False
+        try:
+            return self._step_fused_ptrs(ptrs, keepalive, False)
+        finally:
+            self.validate = saved
+
+    def step_graph(self, actions) -> "StepGraph":
+        """Capture Env.step into CUDA graphs over the given action buffer(s)."""
+        return StepGraph(self, actions)
+
     @property
     def _any_obs_noise(self) -> bool:
         return any(a.obs_noise_std > 0.0 for a in self.agents)
@@ -362,6 +375,66 @@ class Env:
 
 Environment = Env
 _BASE_INFO = Scenario.info
+
+
+class StepGraph:
+    """Env.step as CUDA-graph replays — the launch-overhead-free stepping mode.
+
+    For built-in scenarios: each action buffer in `actions` (one or more
+    (A, B, 2) float32 device tensors, read in place at every replay) gets a
+    captured graph of one fused step; step(i) replays graph i.  Outputs are
+    static tensors owned by the graph and overwritten by the next replay of
+    the same graph.  Semantics are Env.step's with validate=False (no NaN
+    scan): results are bit-identical to eager stepping.  Scenarios that draw
+    from the Env's stream every step (discovery) get one graph per half of
+    the double-buffered Philox state.
+    """
+
+    def __init__(self, env: Env, actions):
+        if not env.fused:
+            raise ContractViolation("StepGraph needs a built-in (fused) scenario")
+        acts = [actions] if isinstance(actions, torch.Tensor) else list(actions)
+        A, B = len(env.agents), env.batch_size
+        for t in acts:
+            if (t.device != env.device or t.dtype != torch.float32 or tuple(t.shape) != (A, B, 2)
+                    or not t.is_contiguous()):
+                raise ContractViolation(f"StepGraph actions must be contiguous float32 ({A}, {B}, 2) on {env.device}")
+        if (env._needs_host_decode([0] * A) or any(s.comm_dim for s in env.action_specs)
+                or env._any_obs_noise):
+            raise ContractViolation("StepGraph covers continuous, noiseless, unscripted, silent agents")
+        self.env = env
+        self.actions = acts
+        self._rng_mode = bool(env.scenario.advances_rng_per_step)
+        sc, world = env.scenario, env.world
+        world.ensure_device_rng()
+        sc.native_handle(world)           # build the descriptor outside capture
+        sc.physics_fused(world)
+        start_cur = world.rng.cur
+        self._graphs: dict = {}
+        self._results: dict = {}
+        stream = torch.cuda.Stream(env.device)
+        stream.wait_stream(torch.cuda.current_stream(env.device))
+        for cur in ((0, 1) if self._rng_mode else (start_cur,)):
+            for i, act in enumerate(acts):
+                world.rng.cur = cur
+                g = torch.cuda.CUDAGraph()
+                base, stride = act.data_ptr(), B * 8
+                ptrs = [base + a * stride for a in range(A)]
+                with torch.cuda.stream(stream), torch.cuda.graph(g, stream=stream):
+                    res = env._capture_step(ptrs, act)
+                self._graphs[(cur, i)] = g
+                self._results[(cur, i)] = res
+        torch.cuda.current_stream(env.device).wait_stream(stream)
+        world.rng.cur = start_cur
+
+    def step(self, i: int = 0) -> StepResult:
+        """Replay the step reading actions[i]; returns its static outputs."""
+        rng = self.env.world.rng
+        key = (rng.cur, i)
+        self._graphs[key].replay()
+        if self._rng_mode:
+            rng.flip()
+        return self._results[key]
 
 
 def _make_world(scenario: Scenario, batch_size: int, rng, device) -> World:

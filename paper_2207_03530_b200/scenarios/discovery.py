@@ -17,6 +17,7 @@ import numpy as np
 import torch
 
 from .. import _native as N
+from .._numerics import sqrt_le_bound
 from ..core import Agent, World
 from ..shapes import Sphere
 from . import register
@@ -74,6 +75,8 @@ class Discovery(FusedScenario):
         r = world.entities[0].shape.radius
         d.sc[0] = f32(r + r)
         d.sc[1] = f32(self.cover_dist)
+        d.sc[2] = sqrt_le_bound(d.sc[0])
+        d.sc[3] = sqrt_le_bound(d.sc[1])
         d.si[0] = int(self.quorum)
         lo = np.asarray((-0.9, -0.9), dtype=np.float64)
         hi = np.asarray((0.9, 0.9), dtype=np.float64)

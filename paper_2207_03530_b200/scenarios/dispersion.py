@@ -18,6 +18,7 @@ import numpy as np
 import torch
 
 from .. import _native as N
+from .._numerics import sqrt_le_bound
 from ..core import Agent, World
 from ..shapes import Sphere
 from . import register
@@ -67,6 +68,7 @@ class Dispersion(FusedScenario):
 
     def fill_constants(self, world, d):
         d.sc[1] = f32(self.eat_dist)
+        d.sc[3] = sqrt_le_bound(d.sc[1])
 
     # reference aux state, read back from the device
     @property

@@ -17,6 +17,7 @@ import ctypes
 import numpy as np
 
 from .. import _native as N
+from .._numerics import sqrt_le_bound
 from ..core import Agent, Entity, World
 from ..sensors import Lidar
 from ..shapes import Sphere, min_contact_distance
@@ -86,9 +87,13 @@ class Flocking(FusedScenario):
         d.sc[0] = f32(min_contact_distance(a0.shape, a0.shape) + 0.0)
         d.sc[1] = f32(min_contact_distance(a0.shape, rock.shape) + 0.0) if rock else 0.0
         d.sc[2] = f32(self.collision_penalty)
+        d.sc[3] = sqrt_le_bound(d.sc[0])
+        d.sc[4] = sqrt_le_bound(d.sc[1]) if rock else -1.0
         d.si[4] = self.n_obstacles
         d.sd[0] = a0.shape.radius * a0.shape.radius
         d.sd[1] = rock.shape.radius * rock.shape.radius if rock else 0.0
+        d.sd[2] = a0.shape.radius
+        d.sd[3] = rock.shape.radius if rock else 0.0
         if self.lidar is not None:
             lid = self.lidar
             table = np.ascontiguousarray(lid.direction_table(), dtype=np.float64)

@@ -11,6 +11,7 @@ import numpy as np
 import torch
 
 from .. import _native as N
+from .._numerics import sqrt_le_bound
 from ..core import Agent, World
 from ..shapes import Sphere, min_contact_distance
 from . import register
@@ -55,8 +56,10 @@ class SimpleSpread(FusedScenario):
 
     def fill_constants(self, world, d):
         a = world.agents
-        d.sc[0] = f32(min_contact_distance(a[0].shape, a[0].shape) + 0.0)   # common.touching
+        thr = f32(min_contact_distance(a[0].shape, a[0].shape) + 0.0)   # common.touching
+        d.sc[0] = thr
         d.sc[1] = f32(self.collision_penalty)
+        d.sc[2] = sqrt_le_bound(thr)
 
     def heuristic_action(self, agent_index: int, obs):
         target = obs[:, 4 + 2 * agent_index: 6 + 2 * agent_index]
