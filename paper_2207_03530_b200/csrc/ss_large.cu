@@ -62,6 +62,7 @@ struct WarpSmem {
   float2* vel;     // [NA]
   float2* lm;      // [NL] landmark positions
   float* tmpl;     // template (16-byte aligned)
+  float* tmpl_shift;  // discovery: tmpl slots shifted by one (slot s holds slot s+1)
   float* tmp;      // [2*NL] per-landmark scratch
   uint32_t* bits;  // [4] landmark flag words
 };
@@ -71,7 +72,7 @@ __host__ __device__ inline int round4(int n) { return (n + 3) & ~3; }
 // First region: discovery's float2 template [2 + NL + NA], or dispersion's
 // float template [4 + 3 NL] followed by its agent positions [NA] (float2).
 __host__ __device__ inline int tmpl_floats(int NA, int NL) {
-  const int disc = 2 * (2 + NL + NA);
+  const int disc = 2 * round4(2 * (2 + NL + NA));   // template + one-slot-shifted copy
   const int disp = round4(4 + 3 * NL) + 2 * NA;
   return round4(disc > disp ? disc : disp);
 }
@@ -84,6 +85,7 @@ SS_DEV WarpSmem carve(float* base, int NA, int NL, bool discovery) {
   WarpSmem w;
   const int t = tmpl_floats(NA, NL);
   w.tmpl = base;
+  w.tmpl_shift = base + round4(2 * (2 + NL + NA));
   float* p = base + t;
   w.vel = reinterpret_cast<float2*>(p);
   p += round4(2 * NA);
@@ -134,20 +136,23 @@ SS_DEV void agents_physics(const LargeArgs& a, float2* pos, float2* vel, int64_t
       }
     }
     if (PAIRS) {
+      // The squared distance is symmetric ((-x)^2 == x^2 bitwise), so the
+      // activity test runs once per (j, k) on pk - pj; the oriented, exact
+      // contact (the reference's operand order) only in the rare active case.
       for (int j = 0; j < a.NA; ++j) {
         const float2 pj = pos[j];
 #pragma unroll
         for (int t = 0; t < T; ++t) {
           const int k = lane + 32 * t;
-          if (k >= a.NA || j == k) continue;
-          const float sign = ((j + k) & 1) ? -1.0f : 1.0f;
-          float cx, cy;
-          if (j < k) {
-            if (contact_force(pj.x, pj.y, px[t], py[t], a.dmin, a.d2_act, sign, a.ph.ck, a.ph.k, cx, cy)) {
+          const float x = fsub(px[t], pj.x), y = fsub(py[t], pj.y);
+          if (sqnorm(x, y) <= a.d2_act && j != k && k < a.NA) {
+            const float sign = ((j + k) & 1) ? -1.0f : 1.0f;
+            float cx, cy;
+            if (j < k) {
+              contact_force(pj.x, pj.y, px[t], py[t], a.dmin, a.d2_act, sign, a.ph.ck, a.ph.k, cx, cy);
               fx[t] = fsub(fx[t], cx); fy[t] = fsub(fy[t], cy);
-            }
-          } else {
-            if (contact_force(px[t], py[t], pj.x, pj.y, a.dmin, a.d2_act, sign, a.ph.ck, a.ph.k, cx, cy)) {
+            } else {
+              contact_force(px[t], py[t], pj.x, pj.y, a.dmin, a.d2_act, sign, a.ph.ck, a.ph.k, cx, cy);
               fx[t] = fadd(fx[t], cx); fy[t] = fadd(fy[t], cy);
             }
           }
@@ -186,7 +191,10 @@ struct ChunkWalk {
   }
   SS_DEV void advance(int nch, int64_t stride) {
     c += 32;
-    while (c >= nch) { c -= nch; ++r; rowp += stride; }
+    if (c >= nch) {
+      c -= nch; ++r; rowp += stride;
+      while (c >= nch) { c -= nch; ++r; rowp += stride; }   // only when nch < 32
+    }
   }
 };
 
@@ -295,7 +303,15 @@ __global__ void __launch_bounds__(32 * kLargeWarps) k_discovery(const LargeArgs 
   if (a.mode & SS_DO_OBS) {
     // row(k) = [x, y, vx, vy, (point_i - a_k)_i, (a_o - a_k)_{o != k}]
     // template slots: tmpl2[2 + i] = point_i, tmpl2[2 + NL + o] = a_o
+    // Row k skips agent k's own slot: template slot s for s < 2 + NL + k,
+    // slot s + 1 beyond it.  tmpl_shift holds the template shifted by one
+    // slot, so every chunk is one 16-byte shared load from either copy
+    // (only the chunk straddling the skip mixes the two).
     const float2* t2 = reinterpret_cast<const float2*>(sm.tmpl);
+    const float2* t2s = reinterpret_cast<const float2*>(sm.tmpl_shift);
+    const int nslot = 2 + a.NL + a.NA;
+    for (int s = lane; s + 1 < nslot; s += 32) reinterpret_cast<float2*>(sm.tmpl_shift)[s] = t2[s + 1];
+    __syncwarp();
     const int first_agent_slot = 2 + a.NL;
     const int slots = a.O >> 1;
     const int nch = slots / (VEC / 2);          // chunks per row
@@ -303,24 +319,31 @@ __global__ void __launch_bounds__(32 * kLargeWarps) k_discovery(const LargeArgs 
     ChunkWalk w(lane, nch, a.obs + e * a.O, a.obs_stride);
     for (int idx = lane; idx < total; idx += 32) {
       const float2 pk = sm.pos[w.r];
-      float2 out[VEC / 2];
-#pragma unroll
-      for (int h = 0; h < VEC / 2; ++h) {
-        const int s = w.c * (VEC / 2) + h;
+      const int skip = first_agent_slot + w.r;   // first slot served from the shifted copy
+      if (VEC == 4) {
+        const int s0 = 2 * w.c;
+        float4 v;
+        if (w.c == 0) {
+          const float2 vk = sm.vel[w.r];
+          v = make_float4(pk.x, pk.y, vk.x, vk.y);
+        } else if (s0 + 1 < skip || s0 >= skip) {
+          const float4 q = reinterpret_cast<const float4*>(s0 >= skip ? t2s : t2)[w.c];
+          v = make_float4(fsub(q.x, pk.x), fsub(q.y, pk.y), fsub(q.z, pk.x), fsub(q.w, pk.y));
+        } else {
+          const float2 q0 = t2[s0], q1 = t2s[s0 + 1];
+          v = make_float4(fsub(q0.x, pk.x), fsub(q0.y, pk.y), fsub(q1.x, pk.x), fsub(q1.y, pk.y));
+        }
+        __stcs(reinterpret_cast<float4*>(w.rowp) + w.c, v);
+      } else {
+        const int s = w.c;
         float2 v;
         if (s == 0) v = pk;
         else if (s == 1) v = sm.vel[w.r];
         else {
-          const int src = (s >= first_agent_slot && s - first_agent_slot >= w.r) ? s + 1 : s;
-          const float2 q = t2[src];
+          const float2 q = s >= skip ? t2s[s] : t2[s];
           v = make_float2(fsub(q.x, pk.x), fsub(q.y, pk.y));
         }
-        out[h] = v;
-      }
-      if (VEC == 4) {
-        __stcs(reinterpret_cast<float4*>(w.rowp) + w.c, make_float4(out[0].x, out[0].y, out[VEC / 2 - 1].x, out[VEC / 2 - 1].y));
-      } else {
-        __stcs(reinterpret_cast<float2*>(w.rowp) + w.c, out[0]);
+        __stcs(reinterpret_cast<float2*>(w.rowp) + w.c, v);
       }
       w.advance(nch, a.obs_stride);
     }

@@ -66,6 +66,30 @@ SS_DEV void warp_flush(float* __restrict__ dst, int nvalid, int O, float* __rest
   __syncwarp();
 }
 
+// Flush staged rows whose per-lane stride P is padded to an odd number of
+// floats (conflict-free row writes for any O).  With O % 4 == 0 each 16-byte
+// output chunk lies inside one row: 4 scalar shared loads, one float4 store.
+SS_DEV void warp_flush_padded(float* __restrict__ dst, int nvalid, int O, int P,
+                              const float* __restrict__ sbuf) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+  const int n = nvalid * O;
+  if ((O & 3) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
+    const int O4 = O >> 2;
+    for (int q = lane; q < (n >> 2); q += 32) {
+      const int r = q / O4, j = (q - r * O4) << 2;
+      const float* s = sbuf + r * P + j;
+      __stcs(reinterpret_cast<float4*>(dst) + q, make_float4(s[0], s[1], s[2], s[3]));
+    }
+  } else {
+    for (int i = lane; i < n; i += 32) {
+      const int r = i / O;
+      __stcs(dst + i, sbuf[r * P + (i - r * O)]);
+    }
+  }
+  __syncwarp();
+}
+
 // decode_action's continuous branch (env.py:96-98) unless the host already
 // produced final forces.
 SS_DEV float decode_axis(float raw, const SsEntityDesc& d, int raw_forces) {
@@ -335,6 +359,35 @@ SS_DEV bool ray_may_hit(float fx, float fy, float dx, float dy, const RayScreen&
   return true;
 }
 
+// Screen all rays against one circle: bit m set when ray m may hit.
+SS_DEV uint32_t ray_mask(float fx, float fy, const float2* dirs, int n_rays, const RayScreen& s) {
+  const float f2 = fx * fx + fy * fy;
+  if (!(f2 <= s.reach2)) return 0u;
+  const bool outside = f2 - s.r2 > 1e-4f;
+  uint32_t mask = 0u;
+  for (int m = 0; m < n_rays; ++m) {
+    const float2 d = dirs[m];
+    const float cr = fx * d.y - fy * d.x;
+    const float b = fx * d.x + fy * d.y;
+    const bool may = fabsf(cr) <= s.rr && !(outside && b > 1e-4f);
+    mask |= (uint32_t)may << m;
+  }
+  return mask;
+}
+
+// Exact float64 tests for the screened-in rays of one circle; per-ray minima
+// live in shared memory (best[m * kSmallThreads]), so the divergent work is
+// proportional to the number of surviving (ray, circle) pairs, not n_rays.
+SS_DEV void ray_hits(uint32_t mask, double ox, double oy, const double* dir_table, double cx,
+                     double cy, double r2, double* best) {
+  while (mask) {
+    const int m = __ffs(mask) - 1;
+    mask &= mask - 1u;
+    const double t = ray_circle(ox, oy, dir_table[2 * m], dir_table[2 * m + 1], cx, cy, r2);
+    best[m * kSmallThreads] = fmin(best[m * kSmallThreads], t);
+  }
+}
+
 struct FlockLidarK {
   double r2_agent, r2_rock;
   RayScreen agent, rock;
@@ -351,10 +404,19 @@ inline RayScreen make_screen(double r, double max_range) {
 
 template <int NA>
 __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_flocking(const SmallArgs a, const FlockLidarK lk) {
-  extern __shared__ __align__(16) float smem[];
+  extern __shared__ __align__(16) float smem_raw[];
   if (a.guard && *a.guard) return;
   const int NO = a.si[4];
   const int O = a.obs_dim;
+  // shared memory: [per-ray best hits: n_rays x kSmallThreads doubles]
+  //                [float32 ray directions: n_rays (padded to even) float2]
+  //                [per-warp obs staging: kSmallThreads x O floats]
+  double* sbest = reinterpret_cast<double*>(smem_raw);
+  float2* sdir = reinterpret_cast<float2*>(sbest + a.n_rays * kSmallThreads);
+  float* smem = reinterpret_cast<float*>(sdir + ((a.n_rays + 1) & ~1));
+  if (threadIdx.x < a.n_rays)
+    sdir[threadIdx.x] = make_float2((float)a.ray_dir[2 * threadIdx.x], (float)a.ray_dir[2 * threadIdx.x + 1]);
+  __syncthreads();
   const int64_t B = a.s.B;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = e < B;
@@ -441,8 +503,9 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_flocking(const
   }
   if (valid && (a.mode & SS_DO_DONE)) a.done[e] = (uint8_t)(steps >= a.ph.max_steps);
   if (a.mode & SS_DO_OBS) {
-    float* sbuf = smem + (threadIdx.x >> 5) * (32 * O);
-    float* row = sbuf + (threadIdx.x & 31) * O;
+    const int P = O | 1;   // odd per-lane stride: conflict-free row writes
+    float* sbuf = smem + (threadIdx.x >> 5) * (32 * P);
+    float* row = sbuf + (threadIdx.x & 31) * P;
     const int64_t e0 = e - (threadIdx.x & 31);
     const int nvalid = (int)min((int64_t)32, B - e0);
 #pragma unroll
@@ -465,6 +528,24 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_flocking(const
           // entity except the emitter; nearest hit, capped at max_range.
           const double ox = (double)px[i], oy = (double)py[i];
           const float rot_i = a.attach_rot ? a.s.rot[i * B + e].x : 0.0f;
+          if (rot_i == 0.0f) {
+            double* best = sbest + threadIdx.x;
+            for (int m = 0; m < a.n_rays; ++m) best[m * kSmallThreads] = __longlong_as_double(0x7ff0000000000000LL);
+#pragma unroll
+            for (int o = 0; o < NA; ++o) {
+              if (o == i) continue;
+              const uint32_t mk = ray_mask(px[i] - px[o], py[i] - py[o], sdir, a.n_rays, lk.agent);
+              ray_hits(mk, ox, oy, a.ray_dir, (double)px[o], (double)py[o], lk.r2_agent, best);
+            }
+#pragma unroll
+            for (int r = 0; r < kFlockMaxRocks; ++r) {
+              if (r < NO) {
+                const uint32_t mk = ray_mask(px[i] - rx[r], py[i] - ry[r], sdir, a.n_rays, lk.rock);
+                ray_hits(mk, ox, oy, a.ray_dir, (double)rx[r], (double)ry[r], lk.r2_rock, best);
+              }
+            }
+            for (int m = 0; m < a.n_rays; ++m) row[c + m] = (float)fmin(best[m * kSmallThreads], a.lidar_range);
+          } else
           for (int m = 0; m < a.n_rays; ++m) {
             double dx, dy;
             if (rot_i == 0.0f) { dx = a.ray_dir[2 * m]; dy = a.ray_dir[2 * m + 1]; }
@@ -490,7 +571,7 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_flocking(const
           }
         }
       }
-      if (nvalid > 0) warp_flush(a.obs + i * a.obs_stride + e0 * O, nvalid, O, sbuf);
+      if (nvalid > 0) warp_flush_padded(a.obs + i * a.obs_stride + e0 * O, nvalid, O, P, sbuf);
     }
   }
 }
@@ -556,7 +637,20 @@ int launch_small(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_
       a.ray_start = w.d.lidar_start;
       a.ray_span = w.d.lidar_span;
       a.ray_dir = w.d_lidar_dirs;
-#define SS_CASE(n) case n: k_flocking<n><<<grid, kSmallThreads, shmem, st>>>(a, lk); break;
+      if (a.n_rays > 32) {
+        set_error("fused flocking lidar supports at most 32 rays");
+        return SS_ERR_UNSUPPORTED;
+      }
+      const size_t fshmem = (size_t)kSmallThreads * (w.d.obs_dim | 1) * sizeof(float) +
+                            (size_t)a.n_rays * kSmallThreads * sizeof(double) +
+                            (size_t)((a.n_rays + 1) & ~1) * sizeof(float2);
+#define SS_CASE(n)                                                                          \
+  case n:                                                                                   \
+    if (fshmem > 48 * 1024)                                                                 \
+      cudaFuncSetAttribute(k_flocking<n>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                           (int)fshmem);                                                    \
+    k_flocking<n><<<grid, kSmallThreads, fshmem, st>>>(a, lk);                              \
+    break;
       switch (NA) { SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) }
 #undef SS_CASE
       break;
