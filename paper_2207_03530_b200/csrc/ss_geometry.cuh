@@ -15,12 +15,11 @@ SS_DEV V2 vmul(V2 a, float s) { return v2(fmul(a.x, s), fmul(a.y, s)); }
 SS_DEV float vdot(V2 a, V2 b) { return fadd(fmul(a.x, b.x), fmul(a.y, b.y)); }
 SS_DEV float clip01(float t) { return fminf(fmaxf(t, 0.0f), 1.0f); }
 
-// f32 cos/sin of a float32 angle.  For rot == 0 (every BASELINE config) the
-// result is exact; for other angles numpy's SIMD f32 sin/cos may differ by
-// 1 ulp.
+// np.cos / np.sin of a float32 angle, bit-exact (ss_math.cuh np_sincosf).
 SS_DEV void cos_sin(float rot, float& ca, float& sa) {
   if (rot == 0.0f) { ca = 1.0f; sa = rot; return; }
-  sincosf(rot, &sa, &ca);
+  ca = np_cosf(rot);
+  sa = np_sinf(rot);
 }
 
 // segment_endpoints (geometry.py:21-26); half is a Python double.

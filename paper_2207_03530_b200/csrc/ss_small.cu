@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_transport(cons
   if (valid && (a.mode & SS_DO_PHYSICS)) {
     prot = a.s.rot[NA * B + e].x;
     float ca, sa;
-    if (prot == 0.0f) { ca = 1.0f; sa = prot; } else { sincosf(prot, &sa, &ca); }
+    if (prot == 0.0f) { ca = 1.0f; sa = prot; } else { ca = np_cosf(prot); sa = np_sinf(prot); }
     const double hx = a.sd[0], hy = a.sd[1];
     float fx[NA + 1], fy[NA + 1];
 #pragma unroll
