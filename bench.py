@@ -62,6 +62,19 @@ WORKLOADS = {
 }
 
 
+def ncu_traffic(scenario: str, envs: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the fused
+    kernel from the committed ncu --set full capture (profiles/r01), if that
+    capture was taken at this batch size; else None."""
+    p = ROOT / "profiles" / "r01" / "ncu_traffic.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text()).get(scenario)
+    if not d or d["envs"] != envs:
+        return None
+    return d["dram_bytes_per_launch"]
+
+
 def peaks() -> dict:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -248,12 +261,14 @@ def run_b200(args, rank, world, local) -> None:
     K, W = args.steps, args.warmup
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
-    # a pool of distinct action sets, cycled; the pool spans > 2x L2 so no
-    # step reads actions another recent step left in L2
+    # a pool of distinct action sets, cycled; together they span > 2x L2 (or
+    # one set alone exceeds L2), so no step reads actions left in L2
     set_bytes = A * B * 8
-    pool = max(2, min(K + W, -(-2 * 126_000_000 // set_bytes)))
+    pool = 1 if set_bytes > 126_000_000 else max(2, min(8, -(-2 * 126_000_000 // set_bytes)))
     acts = [torch.rand((A, B, 2), device=dev, generator=gen).mul_(2.0).sub_(1.0) for _ in range(pool)]
     stream = torch.cuda.current_stream(dev)
+    # Env.step as CUDA-graph replays (one fused launch each, no Python in the loop)
+    graph = env.step_graph(acts)
 
     # ---- kernel-path throughput (device-resident inputs) -------------------
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
@@ -262,19 +277,19 @@ def run_b200(args, rank, world, local) -> None:
         # clock soak: untimed steps so nvidia-smi sees the loaded clocks
         t_soak, n = time.perf_counter(), 0
         while time.perf_counter() - t_soak < args.soak:
-            env.step(acts[n % pool])
+            graph.step(n % pool)
             n += 1
             if n % 64 == 0:
                 torch.cuda.synchronize(dev)
         for t in range(W):
-            env.step(acts[t % pool])
+            graph.step(t % pool)
         barrier(world, dev)
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
         for k in range(K):
             starts[k].record(stream)
-            env.step(acts[(W + k) % pool])
+            graph.step((W + k) % pool)
             ends[k].record(stream)
         t1.record(stream)
         torch.cuda.synchronize(dev)
@@ -287,6 +302,11 @@ def run_b200(args, rank, world, local) -> None:
     achieved = bpe * B / (ms_launch / 1e3) / 1e9
 
     # ---- end to end through the public API with host buffers --------------
+    # the reference-facing call: Env.step with validation on (NaN scan +
+    # guard), host actions in, observations / rewards / dones back to host
+    del graph
+    env_e2e = Env(create_scenario(scen, **ov), B, seed=0, device=dev, validate=True,
+                  env_offset=rank * B, global_batch=world * B)
     E2E_K = max(3, min(K, 10))
     host_acts = [[torch.from_numpy(np.random.default_rng(7 + k).uniform(-1, 1, (B, 2)).astype(np.float32)).pin_memory()
                   for _ in range(A)] for k in range(E2E_K + 1)]
@@ -295,7 +315,7 @@ def run_b200(args, rank, world, local) -> None:
     done_h = torch.empty(B, dtype=torch.bool).pin_memory()
 
     def e2e_step(k):
-        res = env.step(host_acts[k])
+        res = env_e2e.step(host_acts[k])
         for a in range(A):
             obs_h[a].copy_(res.obs[a], non_blocking=True)
         rew_h.copy_(torch.stack(res.rewards), non_blocking=True)
@@ -338,9 +358,12 @@ def run_b200(args, rank, world, local) -> None:
             "data": "synthetic uniform actions in [-1,1]; env state from the scenario's reset distribution",
             "config": {"workload": f"{scen} {ov}, {B} envs per GPU", "scenario": scen,
                        "envs_per_gpu": B, "global_envs": world * B, "agents": A, "obs_dim": O,
-                       "l2": "working set > L2 (no flush needed)" if bpe * B > 126e6 else "L2-resident"},
+                       "l2": "working set > L2 (no flush needed)" if bpe * B > 126e6 else "L2-resident",
+                       "stepping": "Env.step_graph: CUDA-graph replay of the fused step, "
+                                   f"{pool} action buffer(s) cycled; e2e uses eager Env.step(validate=True)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                         "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                         "frac": achieved / pk["hbm_gbs"], "traffic": ncu_traffic(scen, B),
+                         "traffic_source": "profiles/r01/ncu_traffic.json (ncu --set full, one launch)",
                          "bytes_per_env_step": bpe, "kernel_ms": ms_launch, "peak_source": pk["source"]},
             "e2e": {"value": e2e_value, "unit": "agent-steps/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
