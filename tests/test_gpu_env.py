@@ -200,6 +200,35 @@ def test_full_size_sampled_envs_match_oracle(cuda, name, B):
         np.testing.assert_array_equal(torch.stack(r.rewards).cpu().numpy()[:, idx], np.stack(rew))
 
 
+def test_bulk_copy_pipeline_matches_oracle(cuda):
+    """The opt-in cp.async.bulk pipeline (SS_PIPE=1, read once per process)
+    runs in a subprocess and must match the oracle bit-for-bit."""
+    import subprocess
+    import sys
+
+    code = """
+import sys; sys.path[:0] = [%r, %r]
+import numpy as np, torch
+import golden_util as G, paper_2207_03530_b200 as S
+from oracle import swarm_oracle as O
+B = 1000
+e = S.Env(S.create_scenario("simple_spread"), B, seed=5, device="cuda", validate=False)
+o = O.OracleEnv("simple_spread", B, seed=5)
+for plan in G.pregen_actions(3, B, 12, 6):
+    r = e.step(torch.from_numpy(np.stack(plan)).cuda())
+    obs, rew, done = o.step(plan)
+    for x, y in zip(r.obs, obs): np.testing.assert_array_equal(x.cpu().numpy(), y)
+    np.testing.assert_array_equal(torch.stack(r.rewards).cpu().numpy(), np.stack(rew))
+    np.testing.assert_array_equal(r.dones.cpu().numpy(), done)
+print("PIPE_OK")
+""" % (str(G.GOLDEN.parents[1]), str(G.GOLDEN.parent))
+    import os
+
+    res = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, SS_PIPE="1"),
+                         capture_output=True, text=True, timeout=300)
+    assert "PIPE_OK" in res.stdout, res.stdout + res.stderr
+
+
 def test_sharded_run_equals_single_run(cuda):
     """Two shards of a 257-env discovery run (separate Envs, each with its
     global offset) equal the unsharded run bitwise, random stream included."""
