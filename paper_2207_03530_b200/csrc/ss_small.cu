@@ -521,12 +521,12 @@ SS_DEV uint32_t ray_mask(float fx, float fy, const float2* dirs, int n_rays, con
 // live in shared memory (best[m * kSmallThreads]), so the divergent work is
 // proportional to the number of surviving (ray, circle) pairs, not n_rays.
 SS_DEV void ray_hits(uint32_t mask, double ox, double oy, const double* dir_table, double cx,
-                     double cy, double r2, double* best) {
+                     double cy, double r2, double* best, int stride = kSmallThreads) {
   while (mask) {
     const int m = __ffs(mask) - 1;
     mask &= mask - 1u;
     const double t = ray_circle(ox, oy, dir_table[2 * m], dir_table[2 * m + 1], cx, cy, r2);
-    best[m * kSmallThreads] = fmin(best[m * kSmallThreads], t);
+    best[m * stride] = fmin(best[m * stride], t);
   }
 }
 
@@ -719,6 +719,171 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_flocking(const
 }
 
 // ---------------------------------------------------------------------------
+// flocking, warp-per-agent mapping: a CTA of NA warps handles 32 envs; warp
+// i owns agent i of those envs (lane = env).  Each thread sums the force on
+// its own agent over the reference's pair order restricted to that agent —
+// (j, i) for j < i subtracted, then (i, j) for agents j > i and the rocks
+// added (dynamics.py:163-180) — reading partners from shared memory, then
+// builds agent i's reward, observation row and lidar scan.  NA x more
+// threads per env than k_flocking: the 100k-env config fills the GPU.
+// sc[5] = f32 agent-agent d_min, sc[6] its squared bound, sc[7] agent-rock
+// d_min, sc[8] its squared bound (uniform radii are a template condition).
+// ---------------------------------------------------------------------------
+template <int NA>
+__global__ void __launch_bounds__(32 * NA) k_flocking_w(const SmallArgs a, const FlockLidarK lk) {
+  extern __shared__ __align__(16) float smem_w[];
+  if (a.guard && *a.guard) return;
+  const int NO = a.si[4];
+  const int O = a.obs_dim;
+  const int P = O | 1;
+  const int lane = threadIdx.x & 31, i = threadIdx.x >> 5;
+  const int64_t B = a.s.B;
+  const int64_t e0 = (int64_t)blockIdx.x * 32;
+  const int64_t e = e0 + lane;
+  const bool valid = e < B;
+  const int nvalid = (int)min((int64_t)32, B - e0);
+  // shared memory: [best: n_rays x 32*NA doubles][dirs: n_rays(+1) float2]
+  //                [agents: NA x 32 float4][static: (1+NO) x 32 float2][rows: NA warps x 32 x P]
+  double* sbest = reinterpret_cast<double*>(smem_w);
+  float2* sdir = reinterpret_cast<float2*>(sbest + a.n_rays * 32 * NA);
+  float4* sag = reinterpret_cast<float4*>(sdir + ((a.n_rays + 1) & ~1));
+  float2* sst = reinterpret_cast<float2*>(sag + NA * 32);
+  float* srow = reinterpret_cast<float*>(sst + (1 + NO) * 32) + i * 32 * P;
+  if (threadIdx.x < a.n_rays)
+    sdir[threadIdx.x] = make_float2((float)a.ray_dir[2 * threadIdx.x], (float)a.ray_dir[2 * threadIdx.x + 1]);
+  float4 me = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (valid) {
+    me = a.s.dyn[i * B + e];
+    sag[i * 32 + lane] = me;
+    for (int k = i; k < 1 + NO; k += NA) sst[k * 32 + lane] = a.s.stat[k * B + e];
+  }
+  __syncthreads();
+  if (valid && (a.mode & SS_DO_PHYSICS)) {
+    const SsEntityDesc& d = a.ents[i];
+    const float2 u = a.act[i][e];
+    float fx = decode_axis(u.x, d, a.raw_forces), fy = decode_axis(u.y, d, a.raw_forces);
+    if (a.ph.has_gravity) { fx = fadd(fx, d.grav_x); fy = fadd(fy, d.grav_y); }
+    const float dmin_aa = a.sc[5], d2_aa = a.sc[6], dmin_ar = a.sc[7], d2_ar = a.sc[8];
+#pragma unroll
+    for (int j = 0; j < NA; ++j) {
+      if (j == i) continue;
+      const float4 q = sag[j * 32 + lane];
+      const float sign = ((i + j) & 1) ? -1.0f : 1.0f;
+      float cx, cy;
+      if (j < i) {
+        if (contact_force(q.x, q.y, me.x, me.y, dmin_aa, d2_aa, sign, a.ph.ck, a.ph.k, cx, cy)) {
+          fx = fsub(fx, cx); fy = fsub(fy, cy);
+        }
+      } else {
+        if (contact_force(me.x, me.y, q.x, q.y, dmin_aa, d2_aa, sign, a.ph.ck, a.ph.k, cx, cy)) {
+          fx = fadd(fx, cx); fy = fadd(fy, cy);
+        }
+      }
+    }
+    for (int r = 0; r < NO; ++r) {
+      const float2 q = sst[(1 + r) * 32 + lane];
+      const float sign = ((i + NA + 1 + r) & 1) ? -1.0f : 1.0f;
+      float cx, cy;
+      if (contact_force(me.x, me.y, q.x, q.y, dmin_ar, d2_ar, sign, a.ph.ck, a.ph.k, cx, cy)) {
+        fx = fadd(fx, cx); fy = fadd(fy, cy);
+      }
+    }
+    integrate_lin(me.x, me.y, me.z, me.w, fx, fy, a.ph.keep, d.inv_m_dt, a.ph.dt, d.max_speed);
+    a.s.dyn[i * B + e] = me;
+  }
+  __syncthreads();                       // all partners read their pre-step positions
+  if (valid) sag[i * 32 + lane] = me;
+  __syncthreads();
+  int64_t steps = 0;
+  if (valid && (a.mode & (SS_DO_COUNT | SS_DO_DONE))) {
+    steps = a.s.step_count[e];
+    if (a.mode & SS_DO_COUNT) { steps += 1; if (i == 0) a.s.step_count[e] = steps; }
+  }
+  const float2 beacon = valid ? sst[lane] : make_float2(0.f, 0.f);
+  if (valid && (a.mode & SS_DO_REWARD)) {
+    const float pen = a.sc[2], thr2_aa = a.sc[3], thr2_ar = a.sc[4];
+    const float gap = norm2(fsub(me.x, beacon.x), fsub(me.y, beacon.y));
+    float ca = 0.0f, cr = 0.0f;
+#pragma unroll
+    for (int o = 0; o < NA; ++o) {
+      if (o == i) continue;
+      const float4 q = sag[o * 32 + lane];
+      ca = fadd(ca, sqnorm(fsub(me.x, q.x), fsub(me.y, q.y)) <= thr2_aa ? 1.0f : 0.0f);
+    }
+    for (int r = 0; r < NO; ++r) {
+      const float2 q = sst[(1 + r) * 32 + lane];
+      cr = fadd(cr, sqnorm(fsub(me.x, q.x), fsub(me.y, q.y)) <= thr2_ar ? 1.0f : 0.0f);
+    }
+    __stcs(a.rew + i * B + e, fsub(-gap, fmul(pen, fadd(ca, cr))));
+  }
+  if (valid && i == 0 && (a.mode & SS_DO_DONE)) a.done[e] = (uint8_t)(steps >= a.ph.max_steps);
+  if (a.mode & SS_DO_OBS) {
+    float* row = srow + lane * P;
+    if (valid) {
+      row[0] = me.x; row[1] = me.y; row[2] = me.z; row[3] = me.w;
+      row[4] = fsub(beacon.x, me.x); row[5] = fsub(beacon.y, me.y);
+      int c = 6;
+      for (int r = 0; r < NO; ++r) {
+        const float2 q = sst[(1 + r) * 32 + lane];
+        row[c] = fsub(q.x, me.x); row[c + 1] = fsub(q.y, me.y); c += 2;
+      }
+#pragma unroll
+      for (int o = 0; o < NA; ++o) {
+        if (o == i) continue;
+        const float4 q = sag[o * 32 + lane];
+        row[c] = fsub(q.x, me.x); row[c + 1] = fsub(q.y, me.y); c += 2;
+      }
+      if (a.n_rays > 0) {
+        const double ox = (double)me.x, oy = (double)me.y;
+        const float rot_i = a.attach_rot ? a.s.rot[i * B + e].x : 0.0f;
+        const int stride = 32 * NA;
+        double* best = sbest + threadIdx.x;
+        if (rot_i == 0.0f) {
+          for (int m = 0; m < a.n_rays; ++m) best[m * stride] = __longlong_as_double(0x7ff0000000000000LL);
+#pragma unroll
+          for (int o = 0; o < NA; ++o) {
+            if (o == i) continue;
+            const float4 q = sag[o * 32 + lane];
+            const uint32_t mk = ray_mask(me.x - q.x, me.y - q.y, sdir, a.n_rays, lk.agent);
+            ray_hits(mk, ox, oy, a.ray_dir, (double)q.x, (double)q.y, lk.r2_agent, best, stride);
+          }
+          for (int r = 0; r < NO; ++r) {
+            const float2 q = sst[(1 + r) * 32 + lane];
+            const uint32_t mk = ray_mask(me.x - q.x, me.y - q.y, sdir, a.n_rays, lk.rock);
+            ray_hits(mk, ox, oy, a.ray_dir, (double)q.x, (double)q.y, lk.r2_rock, best, stride);
+          }
+          for (int m = 0; m < a.n_rays; ++m) row[c + m] = (float)fmin(best[m * stride], a.lidar_range);
+        } else {
+          for (int m = 0; m < a.n_rays; ++m) {
+            const double ang = dadd_rn(dadd_rn(a.ray_start, (double)m * a.ray_span / a.n_rays), (double)rot_i);
+            double dx, dy;
+            sincos(ang, &dy, &dx);
+            double b = __longlong_as_double(0x7ff0000000000000LL);
+            for (int o = 0; o < NA; ++o) {
+              if (o == i) continue;
+              const float4 q = sag[o * 32 + lane];
+              b = fmin(b, ray_circle(ox, oy, dx, dy, (double)q.x, (double)q.y, lk.r2_agent));
+            }
+            for (int r = 0; r < NO; ++r) {
+              const float2 q = sst[(1 + r) * 32 + lane];
+              b = fmin(b, ray_circle(ox, oy, dx, dy, (double)q.x, (double)q.y, lk.r2_rock));
+            }
+            row[c + m] = (float)fmin(b, a.lidar_range);
+          }
+        }
+      }
+    }
+    if (nvalid > 0) warp_flush_padded(a.obs + i * a.obs_stride + e0 * O, nvalid, O, P, srow);
+  }
+}
+
+inline size_t flocking_w_smem(int NA, int NO, int n_rays, int O) {
+  return (size_t)n_rays * 32 * NA * sizeof(double) + (size_t)((n_rays + 1) & ~1) * sizeof(float2) +
+         (size_t)NA * 32 * sizeof(float4) + (size_t)(1 + NO) * 32 * sizeof(float2) +
+         (size_t)NA * 32 * (O | 1) * sizeof(float);
+}
+
+// ---------------------------------------------------------------------------
 // Host-side dispatch
 // ---------------------------------------------------------------------------
 // The bulk-copy pipeline is opt-in (SS_PIPE=1): measured on B200 at 1M envs
@@ -834,6 +999,22 @@ int launch_small(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_
       if (a.n_rays > 32) {
         set_error("fused flocking lidar supports at most 32 rays");
         return SS_ERR_UNSUPPORTED;
+      }
+      static const bool legacy = std::getenv("SS_FLOCK_THREAD_PER_ENV") != nullptr;
+      if (!legacy) {
+        // warp per agent (k_flocking_w): 32 envs per CTA of NA warps
+        const size_t wshmem = flocking_w_smem(NA, w.d.si[4], a.n_rays, w.d.obs_dim);
+        const unsigned wgrid = (unsigned)((B + 31) / 32);
+#define SS_CASE(n)                                                                          \
+  case n:                                                                                   \
+    if (wshmem > 48 * 1024)                                                                 \
+      cudaFuncSetAttribute(k_flocking_w<n>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                           (int)wshmem);                                                    \
+    k_flocking_w<n><<<wgrid, 32 * n, wshmem, st>>>(a, lk);                                  \
+    break;
+        switch (NA) { SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) }
+#undef SS_CASE
+        break;
       }
       const size_t fshmem = (size_t)kSmallThreads * (w.d.obs_dim | 1) * sizeof(float) +
                             (size_t)a.n_rays * kSmallThreads * sizeof(double) +

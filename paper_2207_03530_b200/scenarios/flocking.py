@@ -89,6 +89,11 @@ class Flocking(FusedScenario):
         d.sc[2] = f32(self.collision_penalty)
         d.sc[3] = sqrt_le_bound(d.sc[0])
         d.sc[4] = sqrt_le_bound(d.sc[1]) if rock else -1.0
+        # contact constants of the warp-per-agent kernel (pair table values)
+        d.sc[5] = f32(min_contact_distance(a0.shape, a0.shape))
+        d.sc[6] = sqrt_le_bound(d.sc[5])
+        d.sc[7] = f32(min_contact_distance(a0.shape, rock.shape)) if rock else 0.0
+        d.sc[8] = sqrt_le_bound(d.sc[7]) if rock else -1.0
         d.si[4] = self.n_obstacles
         d.sd[0] = a0.shape.radius * a0.shape.radius
         d.sd[1] = rock.shape.radius * rock.shape.radius if rock else 0.0

@@ -27,7 +27,12 @@ for name in %(names)r:
     A = len(env.agents); O = env.observations()[0].shape[1]
     acts = [torch.rand((A, B, 2), device="cuda:0") * 2 - 1 for _ in range(2)]
     g = env.step_graph(acts)
-    for k in range(10): g.step(k % 2)
+    import time
+    t_end = time.perf_counter() + 0.5          # clock soak before timing
+    k = 0
+    while time.perf_counter() < t_end:
+        g.step(k % 2); k += 1
+        if k % 32 == 0: torch.cuda.synchronize()
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
