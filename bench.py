@@ -152,9 +152,16 @@ def dist_setup(n_gpus: int):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # SS_DIST_BACKEND=gloo lets the multi-rank path be exercised with several
+    # ranks on one GPU (launch logic only); real runs use NCCL, one GPU per rank
+    backend = os.environ.get("SS_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return rank, world, local
@@ -165,7 +172,10 @@ def barrier(world: int, dev) -> None:
     import torch.distributed as dist
 
     if world > 1:
-        dist.barrier(device_ids=[dev.index])
+        if dist.get_backend() == "nccl":
+            dist.barrier(device_ids=[dev.index])
+        else:
+            dist.barrier()
     torch.cuda.synchronize(dev)
 
 
@@ -202,10 +212,8 @@ def cpu_oracle_rate(scen: str, overrides: dict, B: int, steps: int, warmup: int 
 
 
 def _shard_worker(args):
-    scen, overrides, B, steps = args
-    import numpy as np  # noqa: F401
-
-    r = cpu_oracle_rate(scen, overrides, B, steps)
+    scen, overrides, B, steps, warmup = args
+    r = cpu_oracle_rate(scen, overrides, B, steps, warmup)
     return r["seconds"]
 
 
@@ -224,7 +232,7 @@ def run_reference(args, rank, world) -> None:
     # each step: all cores advance their shard one step; time = slowest shard
     ctx = mp.get_context("fork")
     with ctx.Pool(cores) as pool:
-        secs = pool.map(_shard_worker, [(scen, ov, per, total_steps)] * cores)
+        secs = pool.map(_shard_worker, [(scen, ov, per, total_steps, args.warmup)] * cores)
     sec = max(secs)
     envs = per * cores
     value = envs * A * total_steps / sec
@@ -340,13 +348,14 @@ def run_b200(args, rank, world, local) -> None:
                "sample": f"{cb} envs x {args.cpu_steps} steps of the same workload, oracle/swarm_oracle.py "
                          "(numpy restatement pinned bit-exact to the reference), 1 core"}
 
-    if world > 1:
-        import torch.distributed as dist
+    # episode statistics of the e2e rollout, all-reduced over NVLink (NCCL)
+    # once, outside every timed region — the only collective of the run
+    from paper_2207_03530_b200.parallel import EpisodeStats
 
-        # episode-statistics reduce over NVLink (never inside the step)
-        stats = torch.stack([torch.stack(env.step(acts[0]).rewards).sum().double(),
-                             torch.tensor(float(B), device=dev, dtype=torch.float64)])
-        dist.all_reduce(stats)
+    stats = EpisodeStats(B, dev)
+    res = env_e2e.step(host_acts[0])
+    stats.update(res.rewards, res.dones)
+    episode = stats.reduce()
 
     if rank == 0:
         pk = peaks()
@@ -368,6 +377,8 @@ def run_b200(args, rank, world, local) -> None:
             "e2e": {"value": e2e_value, "unit": "agent-steps/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": K,
+            "episode_stats": {"mean_return_1step": episode["mean_return"], "envs": episode["envs"],
+                              "reduced_over_ranks": world},
             "clock_soak_s": args.soak,
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,
