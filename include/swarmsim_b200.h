@@ -205,6 +205,11 @@ int ss_lidar(void* world, const SsBuffers* buf, int32_t agent, const SsLidarDesc
 int ss_cast_ray(void* world, const SsBuffers* buf, int32_t exclude, const float* ox,
                 const float* oy, const double* angle, double max_range, float* out, void* stream);
 
+/* np.cos (want_cos != 0) / np.sin of a float32 array, bit-exact with numpy's
+ * float32 loops (used by the scenario observations of wheel.py:72-73,
+ * balance.py obs, and by Vec2.rotated, batching.py:132-134). */
+int ss_np_trig(const float* x, float* out, int64_t n, int32_t want_cos, void* stream);
+
 /* Function-level seams used by the reference's unit tests. All arrays [n]. */
 /* collision_force (dynamics.py:36-66): force on i and the active mask. */
 int ss_collision_force(const float* pix, const float* piy, const float* pjx, const float* pjy,

@@ -95,13 +95,14 @@ def _declare(lib) -> None:
     lib.ss_check_actions.argtypes = [c_vp, P(c_vp), c_vp, c_vp]
     lib.ss_lidar.argtypes = [c_vp, P(SsBuffers), c_i32, P(SsLidarDesc), c_vp, c_vp]
     lib.ss_cast_ray.argtypes = [c_vp, P(SsBuffers), c_i32, c_vp, c_vp, c_vp, c_f64, c_vp, c_vp]
+    lib.ss_np_trig.argtypes = [c_vp, c_vp, c_i64, c_i32, c_vp]
     lib.ss_collision_force.argtypes = [c_vp, c_vp, c_vp, c_vp, c_f32, c_f32, c_f32, c_f32,
                                        c_vp, c_vp, c_vp, c_i64, c_vp]
     lib.ss_closest_points.argtypes = [c_vp, c_vp, c_i32, c_f64, c_f64, c_vp, c_vp, c_i32,
                                       c_f64, c_f64, c_vp, c_vp, c_i64, c_vp, c_vp]
     for name in ("ss_world_create", "ss_world_destroy", "ss_env_step", "ss_world_step", "ss_reset",
                  "ss_mask_count", "ss_check_actions", "ss_lidar", "ss_cast_ray", "ss_collision_force",
-                 "ss_closest_points"):
+                 "ss_closest_points", "ss_np_trig"):
         getattr(lib, name).restype = c_i32
 
 
@@ -126,7 +127,7 @@ def exported_symbols() -> list[str]:
     return [
         "ss_abi_version", "ss_last_error", "ss_world_create", "ss_world_destroy", "ss_env_step",
         "ss_world_step", "ss_reset", "ss_mask_count", "ss_check_actions", "ss_lidar",
-        "ss_cast_ray", "ss_collision_force", "ss_closest_points",
+        "ss_cast_ray", "ss_collision_force", "ss_closest_points", "ss_np_trig",
     ]
 
 
@@ -156,3 +157,13 @@ def pointer_array(tensors) -> ctypes.Array:
     for i, t in enumerate(tensors):
         arr[i] = None if t is None else t.data_ptr()
     return arr
+
+
+def np_trig(x, want_cos: bool):
+    """np.cos / np.sin of a float32 device tensor, bit-exact (ss_np_trig)."""
+    import torch
+
+    t = x.to(torch.float32).contiguous()
+    out = torch.empty_like(t)
+    check(lib().ss_np_trig(ptr(t), ptr(out), t.numel(), int(want_cos), stream_handle(t.device)))
+    return out

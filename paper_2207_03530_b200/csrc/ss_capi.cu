@@ -35,6 +35,7 @@ int launch_lidar(World& w, const SsBuffers* buf, int agent, const SsLidarDesc* l
                  cudaStream_t st);
 int launch_cast_ray(World& w, const SsBuffers* buf, int exclude, const float* ox, const float* oy,
                     const double* angle, double max_range, float* out, cudaStream_t st);
+int launch_np_trig(const float* x, float* out, int64_t n, int want_cos, cudaStream_t st);
 
 template <class T>
 static int upload(const std::vector<T>& v, T** dst) {
@@ -204,6 +205,11 @@ int ss_lidar(void* world, const SsBuffers* buf, int32_t agent, const SsLidarDesc
   if (agent < 0 || agent >= w->d.n_entities) { set_error("emitter index out of range"); return SS_ERR_CONTRACT; }
   if (lidar->n_rays < 1) { set_error("n_rays must be >= 1"); return SS_ERR_CONTRACT; }
   return launch_lidar(*w, buf, agent, lidar, out, static_cast<cudaStream_t>(stream));
+}
+
+int ss_np_trig(const float* x, float* out, int64_t n, int32_t want_cos, void* stream) {
+  if ((!x || !out) && n > 0) { set_error("null argument"); return SS_ERR_CONTRACT; }
+  return launch_np_trig(x, out, n, want_cos, static_cast<cudaStream_t>(stream));
 }
 
 int ss_cast_ray(void* world, const SsBuffers* buf, int32_t exclude, const float* ox,

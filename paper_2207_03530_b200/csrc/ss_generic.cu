@@ -180,6 +180,18 @@ __global__ void k_closest_points(const float2* pos_i, const float* rot_i, ShapeK
   out_j[i] = make_float2(oj.x, oj.y);
 }
 
+// np.cos / np.sin of a float32 array, bit-exact (ss_math.cuh np_sincosf).
+__global__ void k_np_trig(const float* x, float* out, int64_t n, int want_cos) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = np_sincosf(x[i], want_cos != 0);
+}
+
+int launch_np_trig(const float* x, float* out, int64_t n, int want_cos, cudaStream_t st) {
+  if (n <= 0) return SS_OK;
+  k_np_trig<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, out, n, want_cos);
+  return cuda_status(cudaGetLastError(), "np_trig launch");
+}
+
 struct CheckArgs {
   const float* act[kGenericMaxAgents];
   int64_t n;   // floats per agent

@@ -286,11 +286,13 @@ class Env:
     def _host_decoded(self, raw_actions):
         """Discrete / noisy / scripted agents: final forces computed on device with torch."""
         forces = []
-        for raw, agent, spec in zip(raw_actions, self.agents, self.action_specs):
-            if raw is None:
+        # scripts see the pre-step state and run in agent order, before any
+        # physics (dynamics.py:136-138); a script replaces any raw action
+        decoded = [None if raw is None else decode_action(raw, spec, agent, self.rng)
+                   for raw, agent, spec in zip(raw_actions, self.agents, self.action_specs)]
+        for act, agent in zip(decoded, self.agents):
+            if agent.action_script is not None:
                 act = agent.action_script(agent, self.world)
-            else:
-                act = decode_action(raw, spec, agent, self.rng)
             from .dynamics import _validate_action
 
             _validate_action(agent, act, self.batch_size)

@@ -45,6 +45,15 @@ CONFIGS = [
     ("discovery_5_b32", "discovery", {}, 32, 100, 0),
     ("dispersion_64x64_b4", "dispersion", {"n_agents": 64, "n_food": 64}, 4, 30, 0),
     ("discovery_64_b4", "discovery", {"n_agents": 64}, 4, 30, 0),
+    # the other catalog tasks (generic physics kernel + device hooks)
+    ("wheel_b16", "wheel", {}, 16, 60, 0),
+    ("balance_b16", "balance", {}, 16, 60, 0),
+    ("give_way_b16", "give_way", {}, 16, 60, 0),
+    ("football_b16", "football", {}, 16, 60, 0),
+    ("passage_b16", "passage", {}, 16, 60, 0),
+    ("reverse_transport_b16", "reverse_transport", {}, 16, 60, 0),
+    ("dropout_b16", "dropout", {}, 16, 60, 0),
+    ("waterfall_b16", "waterfall", {}, 16, 60, 0),
 ]
 SEED = 0
 CKPT = (1, 10, 100)
@@ -138,7 +147,8 @@ def run_config(tag, name, overrides, B, steps, rays):
     out["reset_all_rng"] = rng_json(env.rng.state())
     meta = {"tag": tag, "scenario": name, "overrides": overrides, "batch": B, "steps": steps,
             "seed": SEED, "action_seed": SEED + 1, "lidar_rays": rays,
-            "entities": [e.name for e in env.world.entities]}
+            "entities": [e.name for e in env.world.entities],
+            "oracle": name in ("simple_spread", "transport", "flocking", "dispersion", "discovery")}
     return out, meta
 
 
