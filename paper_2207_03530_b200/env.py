@@ -149,6 +149,8 @@ class Env:
         dev = torch.device(device) if device is not None else default_device()
         if dev.type != "cuda":
             raise NativeError("the batched step runs on a CUDA device only (no CPU implementation)")
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
         N.lib()   # fail loudly now if the library is missing
         self.scenario = scenario
         self.batch_size = int(batch_size)
