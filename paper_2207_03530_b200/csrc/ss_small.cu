@@ -78,16 +78,21 @@ SS_DEV void warp_flush_padded(float* __restrict__ dst, int nvalid, int O, int P,
   const int lane = threadIdx.x & 31;
   __syncwarp();
   const int n = nvalid * O;
+  // row = floor(q / O4) through a float reciprocal: (q + 0.5) / O4 sits at
+  // least 0.5 / O4 from an integer and q <= 32 * O, so the float product
+  // (relative error < 2^-22) always truncates to the exact quotient.
   if ((O & 3) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
     const int O4 = O >> 2;
+    const float inv = 1.0f / (float)O4;
     for (int q = lane; q < (n >> 2); q += 32) {
-      const int r = q / O4, j = (q - r * O4) << 2;
+      const int r = __float2int_rz(__fmul_rn(__int2float_rn(q) + 0.5f, inv)), j = (q - r * O4) << 2;
       const float* s = sbuf + r * P + j;
       __stcs(reinterpret_cast<float4*>(dst) + q, make_float4(s[0], s[1], s[2], s[3]));
     }
   } else {
+    const float inv = 1.0f / (float)O;
     for (int i = lane; i < n; i += 32) {
-      const int r = i / O;
+      const int r = __float2int_rz(__fmul_rn(__int2float_rn(i) + 0.5f, inv));
       __stcs(dst + i, sbuf[r * P + (i - r * O)]);
     }
   }
@@ -205,7 +210,10 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_simple_spread(
   const int64_t e = a.e_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = e < B;
   SpreadEnv<NA> v;
+  float2 u[NA];
+  int64_t steps = 0;
   if (valid) {
+    // every global load of the step issued up front
 #pragma unroll
     for (int i = 0; i < NA; ++i) {
       const float4 q = a.s.dyn[i * B + e];
@@ -213,20 +221,18 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_simple_spread(
       const float2 m = a.s.stat[i * B + e];
       v.mx[i] = m.x; v.my[i] = m.y;
     }
+    if (a.mode & SS_DO_PHYSICS) {
+#pragma unroll
+      for (int i = 0; i < NA; ++i) u[i] = a.act[i][e];
+    }
+    if (a.mode & (SS_DO_COUNT | SS_DO_DONE)) steps = a.s.step_count[e];
   }
   if (valid && (a.mode & SS_DO_PHYSICS)) {
-    float2 u[NA];
-#pragma unroll
-    for (int i = 0; i < NA; ++i) u[i] = a.act[i][e];
     v.physics(u, a);
 #pragma unroll
     for (int i = 0; i < NA; ++i) a.s.dyn[i * B + e] = make_float4(v.px[i], v.py[i], v.vx[i], v.vy[i]);
   }
-  int64_t steps = 0;
-  if (valid && (a.mode & (SS_DO_COUNT | SS_DO_DONE))) {
-    steps = a.s.step_count[e];
-    if (a.mode & SS_DO_COUNT) { steps += 1; a.s.step_count[e] = steps; }
-  }
+  if (valid && (a.mode & SS_DO_COUNT)) { steps += 1; a.s.step_count[e] = steps; }
   if (valid && (a.mode & SS_DO_REWARD)) {
     float rew[NA];
     v.rewards(a, rew);
@@ -377,7 +383,10 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_transport(cons
   const bool valid = e < B;
   float px[NA + 1], py[NA + 1], vx[NA + 1], vy[NA + 1];
   float gx = 0.f, gy = 0.f, prot = 0.f;
+  float2 u[NA];
+  int64_t steps = 0;
   if (valid) {
+    // every global load of the step issued up front
 #pragma unroll
     for (int i = 0; i <= NA; ++i) {
       const float4 q = a.s.dyn[i * B + e];
@@ -385,9 +394,14 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_transport(cons
     }
     const float2 g = a.s.stat[e];
     gx = g.x; gy = g.y;
+    if (a.mode & SS_DO_PHYSICS) {
+      prot = a.s.rot[NA * B + e].x;
+#pragma unroll
+      for (int i = 0; i < NA; ++i) u[i] = a.act[i][e];
+    }
+    if (a.mode & (SS_DO_COUNT | SS_DO_DONE)) steps = a.s.step_count[e];
   }
   if (valid && (a.mode & SS_DO_PHYSICS)) {
-    prot = a.s.rot[NA * B + e].x;
     float ca, sa;
     if (prot == 0.0f) { ca = 1.0f; sa = prot; } else { ca = np_cosf(prot); sa = np_sinf(prot); }
     const double hx = a.sd[0], hy = a.sd[1];
@@ -395,9 +409,8 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_transport(cons
 #pragma unroll
     for (int i = 0; i < NA; ++i) {
       const SsEntityDesc& d = a.ents[i];
-      const float2 u = a.act[i][e];
-      fx[i] = decode_axis(u.x, d, a.raw_forces);
-      fy[i] = decode_axis(u.y, d, a.raw_forces);
+      fx[i] = decode_axis(u[i].x, d, a.raw_forces);
+      fy[i] = decode_axis(u[i].y, d, a.raw_forces);
     }
     fx[NA] = 0.0f; fy[NA] = 0.0f;
     if (a.ph.has_gravity) {
@@ -436,11 +449,7 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_transport(cons
       a.s.dyn[i * B + e] = make_float4(px[i], py[i], vx[i], vy[i]);
     }
   }
-  int64_t steps = 0;
-  if (valid && (a.mode & (SS_DO_COUNT | SS_DO_DONE))) {
-    steps = a.s.step_count[e];
-    if (a.mode & SS_DO_COUNT) { steps += 1; a.s.step_count[e] = steps; }
-  }
+  if (valid && (a.mode & SS_DO_COUNT)) { steps += 1; a.s.step_count[e] = steps; }
   if (valid && (a.mode & (SS_DO_REWARD | SS_DO_DONE))) {
     const float gap = norm2(fsub(px[NA], gx), fsub(py[NA], gy));
     if (a.mode & SS_DO_REWARD) {
@@ -530,10 +539,163 @@ SS_DEV void ray_hits(uint32_t mask, double ox, double oy, const double* dir_tabl
   }
 }
 
+// Uniform ray fan (sensors.py:40-43): angle_m = start + m * step, m < n,
+// with 0 < n * step <= 2 pi.  All quantities in units of `step`.
+struct RayFan {
+  float start;      // start angle (rad)
+  float inv_step;   // 1 / step
+  float period;     // 2 pi / step
+  float quarter;    // (pi / 2) / step
+  uint32_t all;     // bits 0..n-1
+  int n;
+};
+
+// atan2 with |error| < 2e-6 rad over all quadrants (checked on the host
+// against libm atan2 on 2e7 angles); minimax polynomial on [0, 1].
+SS_DEV float fast_atan2(float y, float x) {
+  const float ax = fabsf(x), ay = fabsf(y);
+  const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+  const float t = mx > 0.f ? __fdividef(mn, mx) : 0.f;
+  const float s = __fmul_rn(t, t);
+  float p = -0.01172120f;
+  p = __fmaf_rn(p, s, 0.05265332f);
+  p = __fmaf_rn(p, s, -0.11643287f);
+  p = __fmaf_rn(p, s, 0.19354346f);
+  p = __fmaf_rn(p, s, -0.33262347f);
+  p = __fmaf_rn(p, s, 0.99997726f);
+  float r = __fmul_rn(p, t);
+  if (ay > ax) r = __fsub_rn(1.57079637f, r);
+  if (x < 0.f) r = __fsub_rn(3.14159274f, r);
+  return copysignf(r, y);
+}
+
+// Rays m (0 <= m < n) with lo <= m <= hi.
+SS_DEV uint32_t ray_bits(float lo, float hi, int n) {
+  const int a = max((int)ceilf(fmaxf(lo, -1.0f)), 0);
+  const int b = min((int)floorf(fminf(hi, 64.0f)), n - 1);
+  if (a > b) return 0u;
+  return (0xffffffffu >> (31 - b)) & (0xffffffffu << a);
+}
+
+// Conservative angular screen of one circle against a whole fan: a ray can
+// hit a circle of radius r seen at distance |f| > r only if its angle lies
+// within asin(r / |f|) <= r / sqrt(|f|^2 - r^2) of the bearing to the centre
+// (and then it points towards it).  The window is widened by 0.1% + 0.01
+// ray spacings (>= 2.5e3 x the atan2 / rsqrt / fp32 rounding error) and r by
+// 1e-4, so every ray the exact float64 test could report within max_range
+// is kept; origins on or inside the (widened) rim and windows wider than
+// pi/2 keep every ray.
+SS_DEV uint32_t ray_window(float fx, float fy, const RayFan& fan, const RayScreen& s) {
+  const float f2 = __fadd_rn(__fmul_rn(fx, fx), __fmul_rn(fy, fy));
+  if (!(f2 <= s.reach2)) return 0u;
+  const float q = __fsub_rn(f2, __fmul_rn(s.rr, s.rr));
+  if (!(q > 1e-6f)) return fan.all;
+  const float w = __fmaf_rn(__fmul_rn(__fmul_rn(s.rr, rsqrtf(q)), fan.inv_step), 1.001f, 0.01f);
+  if (!(w < fan.quarter)) return fan.all;
+  float v = __fmul_rn(__fsub_rn(fast_atan2(-fy, -fx), fan.start), fan.inv_step);
+  v = __fsub_rn(v, __fmul_rn(fan.period, floorf(__fdividef(v, fan.period))));
+  return ray_bits(v - w, v + w, fan.n) | ray_bits(v - w + fan.period, v + w + fan.period, fan.n) |
+         ray_bits(v - w - fan.period, v + w - fan.period, fan.n);
+}
+
+// ray_hits with the minima kept as float bits (see lidar_fan_warp).
+SS_DEV void ray_hits_f(uint32_t mask, double ox, double oy, const double2* dirs, double cx, double cy,
+                       double r2, uint32_t* best, int stride) {
+  while (mask) {
+    const int m = __ffs(mask) - 1;
+    mask &= mask - 1u;
+    const double t = ray_circle(ox, oy, dirs[m].x, dirs[m].y, cx, cy, r2);
+    best[m * stride] = min(best[m * stride], __float_as_uint((float)t));
+  }
+}
+
 struct FlockLidarK {
   double r2_agent, r2_rock;
   RayScreen agent, rock;
+  RayFan fan;
+  int fan_ok;   // uniform fan usable (else the per-ray screen)
 };
+
+constexpr int kLidarQueue = 64;    // (lane, target, ray) tests staged per warp and round
+
+// Lidar of agent i for the 32 envs of one warp (k_flocking_w), load-balanced
+// across lanes: each lane screens its env's targets with ray_window, the
+// surviving (env, target, ray) triples are compacted into a per-warp queue
+// (warp prefix sum) and the exact float64 tests are dealt out 32 at a time,
+// so a warp runs ceil(total / 32) test rounds instead of the maximum per-lane
+// count per target.  Minima land in the staged observation rows themselves
+// (best[lane * P + ray], the lidar columns) as float bits (atomicMin on
+// the non-negative float pattern): float(min(t, range)) == min(float(t),
+// float(range)) since rounding is monotone, so the scan stays bit-identical.
+// Warp-collective: every lane of the warp must call it.
+template <int NA>
+SS_DEV void lidar_fan_warp(bool active, int i, int lane, int NO, float mex, float mey,
+                           const float4* sag, const float2* sst, const FlockLidarK& lk,
+                           const double2* sdird, uint32_t* best, int P, uint32_t* queue, int n_rays) {
+  constexpr int NT = NA - 1 + kFlockMaxRocks;
+  uint32_t mk[NT];
+  int cnt = 0;
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    mk[t] = 0u;
+    if (active && (t < NA - 1 || t - (NA - 1) < NO)) {
+      float qx, qy;
+      if (t < NA - 1) {
+        const float4 q = sag[(t < i ? t : t + 1) * 32 + lane];
+        qx = q.x; qy = q.y;
+      } else {
+        const float2 q = sst[(t - (NA - 1) + 1) * 32 + lane];
+        qx = q.x; qy = q.y;
+      }
+      mk[t] = ray_window(__fsub_rn(mex, qx), __fsub_rn(mey, qy), lk.fan, t < NA - 1 ? lk.agent : lk.rock);
+      cnt += __popc(mk[t]);
+    }
+  }
+  for (int m = 0; m < n_rays; ++m) best[lane * P + m] = 0x7f800000u;   // +inf
+  int incl = cnt;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += v;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  const int excl = incl - cnt;
+  for (int base = 0; base < total; base += kLidarQueue) {
+    if (excl < base + kLidarQueue && excl + cnt > base) {
+      int idx = excl;
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        uint32_t m = mk[t];
+        while (m) {
+          const int r = __ffs(m) - 1;
+          m &= m - 1u;
+          if (idx >= base && idx < base + kLidarQueue) queue[idx - base] = (uint32_t)lane | (t << 5) | (r << 9);
+          ++idx;
+        }
+      }
+    }
+    __syncwarp();
+    const int nq = min(kLidarQueue, total - base);
+    for (int k = lane; k < nq; k += 32) {
+      const uint32_t w = queue[k];
+      const int sl = (int)(w & 31u), t = (int)((w >> 5) & 15u), r = (int)(w >> 9);
+      const float4 org = sag[i * 32 + sl];
+      double cx, cy, r2;
+      if (t < NA - 1) {
+        const float4 q = sag[(t < i ? t : t + 1) * 32 + sl];
+        cx = q.x; cy = q.y; r2 = lk.r2_agent;
+      } else {
+        const float2 q = sst[(t - (NA - 1) + 1) * 32 + sl];
+        cx = q.x; cy = q.y; r2 = lk.r2_rock;
+      }
+      const double2 d = sdird[r];
+      const double tt = ray_circle((double)org.x, (double)org.y, d.x, d.y, cx, cy, r2);
+      if (tt < __longlong_as_double(0x7ff0000000000000LL))
+        atomicMin(best + sl * P + r, __float_as_uint((float)tt));
+    }
+    __syncwarp();
+  }
+}
 
 inline RayScreen make_screen(double r, double max_range) {
   RayScreen s;
@@ -729,8 +891,12 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_flocking(const
 // sc[5] = f32 agent-agent d_min, sc[6] its squared bound, sc[7] agent-rock
 // d_min, sc[8] its squared bound (uniform radii are a template condition).
 // ---------------------------------------------------------------------------
+#ifndef SS_FLOCK_WARPS
+#define SS_FLOCK_WARPS 40   // resident warps per SM the register budget is sized for
+#endif
 template <int NA>
-__global__ void __launch_bounds__(32 * NA) k_flocking_w(const SmallArgs a, const FlockLidarK lk) {
+__global__ void __launch_bounds__(32 * NA, (SS_FLOCK_WARPS / NA < 32 ? SS_FLOCK_WARPS / NA : 32))
+    k_flocking_w(const SmallArgs a, const FlockLidarK lk) {
   extern __shared__ __align__(16) float smem_w[];
   if (a.guard && *a.guard) return;
   const int NO = a.si[4];
@@ -742,25 +908,34 @@ __global__ void __launch_bounds__(32 * NA) k_flocking_w(const SmallArgs a, const
   const int64_t e = e0 + lane;
   const bool valid = e < B;
   const int nvalid = (int)min((int64_t)32, B - e0);
-  // shared memory: [best: n_rays x 32*NA doubles][dirs: n_rays(+1) float2]
-  //                [agents: NA x 32 float4][static: (1+NO) x 32 float2][rows: NA warps x 32 x P]
-  double* sbest = reinterpret_cast<double*>(smem_w);
-  float2* sdir = reinterpret_cast<float2*>(sbest + a.n_rays * 32 * NA);
-  float4* sag = reinterpret_cast<float4*>(sdir + ((a.n_rays + 1) & ~1));
-  float2* sst = reinterpret_cast<float2*>(sag + NA * 32);
+  // shared memory: [dirs: n_rays double2][agents: NA x 32 float4][queue: NA x kLidarQueue u32]
+  //                [dirs: n_rays(+1) float2][static: (1+NO) x 32 float2][rows: NA warps x 32 x P]
+  // (the lidar minima are accumulated in the rows' lidar columns)
+  double2* sdird = reinterpret_cast<double2*>(smem_w);
+  float4* sag = reinterpret_cast<float4*>(sdird + a.n_rays);
+  uint32_t* squeue = reinterpret_cast<uint32_t*>(sag + NA * 32);
+  float2* sdir = reinterpret_cast<float2*>(squeue + NA * kLidarQueue);
+  float2* sst = reinterpret_cast<float2*>(sdir + ((a.n_rays + 1) & ~1));
   float* srow = reinterpret_cast<float*>(sst + (1 + NO) * 32) + i * 32 * P;
-  if (threadIdx.x < a.n_rays)
-    sdir[threadIdx.x] = make_float2((float)a.ray_dir[2 * threadIdx.x], (float)a.ray_dir[2 * threadIdx.x + 1]);
+  if (threadIdx.x < a.n_rays) {
+    const double dx = a.ray_dir[2 * threadIdx.x], dy = a.ray_dir[2 * threadIdx.x + 1];
+    sdird[threadIdx.x] = make_double2(dx, dy);
+    sdir[threadIdx.x] = make_float2((float)dx, (float)dy);
+  }
   float4 me = make_float4(0.f, 0.f, 0.f, 0.f);
+  int64_t steps = 0;
+  float2 u = make_float2(0.f, 0.f);
   if (valid) {
+    // every global load of the step issued up front
     me = a.s.dyn[i * B + e];
+    if (a.mode & (SS_DO_COUNT | SS_DO_DONE)) steps = a.s.step_count[e];
+    if (a.mode & SS_DO_PHYSICS) u = a.act[i][e];
     sag[i * 32 + lane] = me;
     for (int k = i; k < 1 + NO; k += NA) sst[k * 32 + lane] = a.s.stat[k * B + e];
   }
   __syncthreads();
   if (valid && (a.mode & SS_DO_PHYSICS)) {
     const SsEntityDesc& d = a.ents[i];
-    const float2 u = a.act[i][e];
     float fx = decode_axis(u.x, d, a.raw_forces), fy = decode_axis(u.y, d, a.raw_forces);
     if (a.ph.has_gravity) { fx = fadd(fx, d.grav_x); fy = fadd(fy, d.grav_y); }
     const float dmin_aa = a.sc[5], d2_aa = a.sc[6], dmin_ar = a.sc[7], d2_ar = a.sc[8];
@@ -794,11 +969,7 @@ __global__ void __launch_bounds__(32 * NA) k_flocking_w(const SmallArgs a, const
   __syncthreads();                       // all partners read their pre-step positions
   if (valid) sag[i * 32 + lane] = me;
   __syncthreads();
-  int64_t steps = 0;
-  if (valid && (a.mode & (SS_DO_COUNT | SS_DO_DONE))) {
-    steps = a.s.step_count[e];
-    if (a.mode & SS_DO_COUNT) { steps += 1; if (i == 0) a.s.step_count[e] = steps; }
-  }
+  if (valid && (a.mode & SS_DO_COUNT)) { steps += 1; if (i == 0) a.s.step_count[e] = steps; }
   const float2 beacon = valid ? sst[lane] : make_float2(0.f, 0.f);
   if (valid && (a.mode & SS_DO_REWARD)) {
     const float pen = a.sc[2], thr2_aa = a.sc[3], thr2_ar = a.sc[4];
@@ -833,43 +1004,56 @@ __global__ void __launch_bounds__(32 * NA) k_flocking_w(const SmallArgs a, const
         const float4 q = sag[o * 32 + lane];
         row[c] = fsub(q.x, me.x); row[c + 1] = fsub(q.y, me.y); c += 2;
       }
-      if (a.n_rays > 0) {
-        const double ox = (double)me.x, oy = (double)me.y;
-        const float rot_i = a.attach_rot ? a.s.rot[i * B + e].x : 0.0f;
-        const int stride = 32 * NA;
-        double* best = sbest + threadIdx.x;
-        if (rot_i == 0.0f) {
-          for (int m = 0; m < a.n_rays; ++m) best[m * stride] = __longlong_as_double(0x7ff0000000000000LL);
+    }
+    if (a.n_rays > 0) {
+      const int c = 6 + 2 * NO + 2 * (NA - 1);
+      const double ox = (double)me.x, oy = (double)me.y;
+      const float rot_i = (valid && a.attach_rot) ? a.s.rot[i * B + e].x : 0.0f;
+      const bool fan = valid && rot_i == 0.0f;
+      uint32_t* wbest = reinterpret_cast<uint32_t*>(srow + c);   // this warp's rows, lidar columns
+      uint32_t* best = wbest + lane * P;
+      const int stride = 1;
+      const float range_f = (float)a.lidar_range;
+      if (lk.fan_ok) {
+        // warp-collective: all lanes, including invalid / rotated ones
+        lidar_fan_warp<NA>(fan, i, lane, NO, me.x, me.y, sag, sst, lk, sdird, wbest, P, squeue + i * kLidarQueue,
+                           a.n_rays);
+        if (fan)
+          for (int m = 0; m < a.n_rays; ++m)
+            best[m] = __float_as_uint(fminf(__uint_as_float(best[m]), range_f));
+      } else if (fan) {
+        for (int m = 0; m < a.n_rays; ++m) best[m * stride] = 0x7f800000u;
 #pragma unroll
+        for (int o = 0; o < NA; ++o) {
+          if (o == i) continue;
+          const float4 q = sag[o * 32 + lane];
+          const uint32_t mk = ray_mask(me.x - q.x, me.y - q.y, sdir, a.n_rays, lk.agent);
+          ray_hits_f(mk, ox, oy, sdird, (double)q.x, (double)q.y, lk.r2_agent, best, stride);
+        }
+        for (int r = 0; r < NO; ++r) {
+          const float2 q = sst[(1 + r) * 32 + lane];
+          const uint32_t mk = ray_mask(me.x - q.x, me.y - q.y, sdir, a.n_rays, lk.rock);
+          ray_hits_f(mk, ox, oy, sdird, (double)q.x, (double)q.y, lk.r2_rock, best, stride);
+        }
+        for (int m = 0; m < a.n_rays; ++m) best[m] = __float_as_uint(fminf(__uint_as_float(best[m]), range_f));
+      }
+      if (valid && !fan) {
+        // attached rotation (sensors.py:121-135): per-ray fp64 angles
+        for (int m = 0; m < a.n_rays; ++m) {
+          const double ang = dadd_rn(dadd_rn(a.ray_start, (double)m * a.ray_span / a.n_rays), (double)rot_i);
+          double dx, dy;
+          sincos(ang, &dy, &dx);
+          double b = __longlong_as_double(0x7ff0000000000000LL);
           for (int o = 0; o < NA; ++o) {
             if (o == i) continue;
             const float4 q = sag[o * 32 + lane];
-            const uint32_t mk = ray_mask(me.x - q.x, me.y - q.y, sdir, a.n_rays, lk.agent);
-            ray_hits(mk, ox, oy, a.ray_dir, (double)q.x, (double)q.y, lk.r2_agent, best, stride);
+            b = fmin(b, ray_circle(ox, oy, dx, dy, (double)q.x, (double)q.y, lk.r2_agent));
           }
           for (int r = 0; r < NO; ++r) {
             const float2 q = sst[(1 + r) * 32 + lane];
-            const uint32_t mk = ray_mask(me.x - q.x, me.y - q.y, sdir, a.n_rays, lk.rock);
-            ray_hits(mk, ox, oy, a.ray_dir, (double)q.x, (double)q.y, lk.r2_rock, best, stride);
+            b = fmin(b, ray_circle(ox, oy, dx, dy, (double)q.x, (double)q.y, lk.r2_rock));
           }
-          for (int m = 0; m < a.n_rays; ++m) row[c + m] = (float)fmin(best[m * stride], a.lidar_range);
-        } else {
-          for (int m = 0; m < a.n_rays; ++m) {
-            const double ang = dadd_rn(dadd_rn(a.ray_start, (double)m * a.ray_span / a.n_rays), (double)rot_i);
-            double dx, dy;
-            sincos(ang, &dy, &dx);
-            double b = __longlong_as_double(0x7ff0000000000000LL);
-            for (int o = 0; o < NA; ++o) {
-              if (o == i) continue;
-              const float4 q = sag[o * 32 + lane];
-              b = fmin(b, ray_circle(ox, oy, dx, dy, (double)q.x, (double)q.y, lk.r2_agent));
-            }
-            for (int r = 0; r < NO; ++r) {
-              const float2 q = sst[(1 + r) * 32 + lane];
-              b = fmin(b, ray_circle(ox, oy, dx, dy, (double)q.x, (double)q.y, lk.r2_rock));
-            }
-            row[c + m] = (float)fmin(b, a.lidar_range);
-          }
+          row[c + m] = (float)fmin(b, a.lidar_range);
         }
       }
     }
@@ -878,8 +1062,9 @@ __global__ void __launch_bounds__(32 * NA) k_flocking_w(const SmallArgs a, const
 }
 
 inline size_t flocking_w_smem(int NA, int NO, int n_rays, int O) {
-  return (size_t)n_rays * 32 * NA * sizeof(double) + (size_t)((n_rays + 1) & ~1) * sizeof(float2) +
-         (size_t)NA * 32 * sizeof(float4) + (size_t)(1 + NO) * 32 * sizeof(float2) +
+  return (size_t)n_rays * sizeof(double2) + (size_t)NA * 32 * sizeof(float4) +
+         (size_t)NA * kLidarQueue * sizeof(uint32_t) +
+         (size_t)((n_rays + 1) & ~1) * sizeof(float2) + (size_t)(1 + NO) * 32 * sizeof(float2) +
          (size_t)NA * 32 * (O | 1) * sizeof(float);
 }
 
@@ -999,6 +1184,19 @@ int launch_small(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_
       if (a.n_rays > 32) {
         set_error("fused flocking lidar supports at most 32 rays");
         return SS_ERR_UNSUPPORTED;
+      }
+      {
+        // uniform fan screen (k_flocking_w): needs 0 < span <= 2 pi
+        const double two_pi = 6.283185307179586, span = w.d.lidar_span;
+        static const bool no_fan = std::getenv("SS_LIDAR_NO_FAN") != nullptr;
+        lk.fan_ok = !no_fan && a.n_rays > 0 && span > 0.0 && span <= two_pi * (1.0 + 1e-12);
+        const double step = a.n_rays > 0 ? span / a.n_rays : 1.0;
+        lk.fan.start = (float)w.d.lidar_start;
+        lk.fan.inv_step = (float)(1.0 / step);
+        lk.fan.period = (float)(two_pi / step);
+        lk.fan.quarter = (float)(0.25 * two_pi / step);
+        lk.fan.n = a.n_rays;
+        lk.fan.all = a.n_rays >= 32 ? 0xffffffffu : ((1u << a.n_rays) - 1u);
       }
       static const bool legacy = std::getenv("SS_FLOCK_THREAD_PER_ENV") != nullptr;
       if (!legacy) {

@@ -1,0 +1,73 @@
+"""Throughput vs number of parallel envs on one GPU (the paper's scaling sweep).
+
+    python tools/batch_sweep.py SCENARIO B1 B2 ... [--steps K]
+
+For each batch size: a fresh Env stepped by CUDA-graph replay of the fused
+step with device-resident random actions (two buffers cycled), 0.3 s clock
+soak, then K timed steps.  Prints one JSON line per size: per-launch median
+kernel time (CUDA events around each replay), ms per step over the whole
+timed loop, env-steps/s, agent-steps/s and the HBM roofline fraction
+(algorithmic bytes per env-step).
+"""
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from bench import WORKLOADS, bytes_per_env_step, peaks  # noqa: E402
+from paper_2207_03530_b200 import Env, create_scenario  # noqa: E402
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("scenario")
+    ap.add_argument("sizes", type=int, nargs="+")
+    ap.add_argument("--steps", type=int, default=50)
+    args = ap.parse_args()
+    scen, ov, _ = WORKLOADS[args.scenario]
+    dev = torch.device("cuda:0")
+    hbm = peaks()["hbm_gbs"]
+    for B in args.sizes:
+        env = Env(create_scenario(scen, **ov), B, seed=0, device=dev, validate=False)
+        A = len(env.agents)
+        O = env.observations()[0].shape[1]
+        bpe = bytes_per_env_step(scen, A, len(env.world.entities) - A, O)
+        acts = [torch.rand((A, B, 2), device=dev) * 2 - 1 for _ in range(2)]
+        g = env.step_graph(acts)
+        t0, n = time.perf_counter(), 0
+        while time.perf_counter() - t0 < 0.3:
+            g.step(n % 2)
+            n += 1
+            if n % 64 == 0:
+                torch.cuda.synchronize()
+        K = args.steps
+        s = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
+        torch.cuda.synchronize()
+        ends = []
+        for k in range(K):
+            s[k].record()
+            g.step(k % 2)
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            ends.append(e)
+        s[K].record()
+        torch.cuda.synchronize()
+        launch = float(np.median([s[k].elapsed_time(ends[k]) for k in range(K)]))
+        total = s[0].elapsed_time(s[K]) / K
+        rate = B / (total / 1e3)
+        print(json.dumps({"scenario": args.scenario, "envs": B, "kernel_ms": launch, "ms_per_step": total,
+                          "env_steps_per_s": rate, "agent_steps_per_s": rate * A,
+                          "bytes_per_env_step": bpe, "hbm_frac": bpe * B / (launch / 1e3) / 1e9 / hbm,
+                          "working_set_mb": bpe * B / 1e6}), flush=True)
+        del g, env
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
