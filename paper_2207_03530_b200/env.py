@@ -12,6 +12,8 @@ VMAS-style aliases: make_env, Environment (= Env), Env.reset_at(mask).
 """
 from __future__ import annotations
 
+import gc
+
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -354,9 +356,9 @@ class Env:
         finally:
             self.validate = saved
 
-    def step_graph(self, actions) -> "StepGraph":
+    def step_graph(self, actions, steps_per_replay: int = 1) -> "StepGraph":
         """Capture Env.step into CUDA graphs over the given action buffer(s)."""
-        return StepGraph(self, actions)
+        return StepGraph(self, actions, steps_per_replay)
 
     @property
     def _any_obs_noise(self) -> bool:
@@ -386,19 +388,25 @@ class StepGraph:
 
     For built-in scenarios: each action buffer in `actions` (one or more
     (A, B, 2) float32 device tensors, read in place at every replay) gets a
-    captured graph of one fused step; step(i) replays graph i.  Outputs are
-    static tensors owned by the graph and overwritten by the next replay of
-    the same graph.  Semantics are Env.step's with validate=False (no NaN
-    scan): results are bit-identical to eager stepping.  Scenarios that draw
-    from the Env's stream every step (discovery) get one graph per half of
-    the double-buffered Philox state.
+    captured graph; step(i) replays graph i.  With steps_per_replay=S > 1 a
+    graph holds S consecutive fused steps reading actions[i], actions[i+1],
+    ... (cyclically) — an open-loop rollout whose S StepResults live in
+    distinct graph-owned buffers (rollout(i)), so the GPU runs the steps back
+    to back without a host launch between them.  Outputs are static tensors
+    owned by the graph and overwritten by its next replay.  Semantics are
+    Env.step's with validate=False (no NaN scan): results are bit-identical
+    to eager stepping.  Scenarios that draw from the Env's stream every step
+    (discovery) get one graph per half of the double-buffered Philox state.
     """
 
-    def __init__(self, env: Env, actions):
+    def __init__(self, env: Env, actions, steps_per_replay: int = 1):
         if not env.fused:
             raise ContractViolation("StepGraph needs a built-in (fused) scenario")
         acts = [actions] if isinstance(actions, torch.Tensor) else list(actions)
         A, B = len(env.agents), env.batch_size
+        S = int(steps_per_replay)
+        if S < 1:
+            raise ContractViolation(f"steps_per_replay must be >= 1, got {steps_per_replay}")
         for t in acts:
             if (t.device != env.device or t.dtype != torch.float32 or tuple(t.shape) != (A, B, 2)
                     or not t.is_contiguous()):
@@ -408,6 +416,7 @@ class StepGraph:
             raise ContractViolation("StepGraph covers continuous, noiseless, unscripted, silent agents")
         self.env = env
         self.actions = acts
+        self.steps_per_replay = S
         self._rng_mode = bool(env.scenario.advances_rng_per_step)
         sc, world = env.scenario, env.world
         world.ensure_device_rng()
@@ -418,27 +427,45 @@ class StepGraph:
         self._results: dict = {}
         stream = torch.cuda.Stream(env.device)
         stream.wait_stream(torch.cuda.current_stream(env.device))
-        for cur in ((0, 1) if self._rng_mode else (start_cur,)):
-            for i, act in enumerate(acts):
-                world.rng.cur = cur
-                g = torch.cuda.CUDAGraph()
-                base, stride = act.data_ptr(), B * 8
-                ptrs = [base + a * stride for a in range(A)]
-                with torch.cuda.stream(stream), torch.cuda.graph(g, stream=stream):
-                    res = env._capture_step(ptrs, act)
-                self._graphs[(cur, i)] = g
-                self._results[(cur, i)] = res
+        # no cyclic GC inside a capture: a collected world handle would call
+        # cudaFree on the capturing thread and invalidate the graph
+        gc_was = gc.isenabled()
+        gc.collect()
+        gc.disable()
+        try:
+            for cur in ((0, 1) if self._rng_mode else (start_cur,)):
+                for i in range(len(acts)):
+                    world.rng.cur = cur       # each captured step flips it in rng mode
+                    g = torch.cuda.CUDAGraph()
+                    results = []
+                    with torch.cuda.stream(stream), torch.cuda.graph(g, stream=stream):
+                        for k in range(S):
+                            act = acts[(i + k) % len(acts)]
+                            base, stride = act.data_ptr(), B * 8
+                            results.append(env._capture_step([base + a * stride for a in range(A)], act))
+                    self._graphs[(cur, i)] = g
+                    self._results[(cur, i)] = results
+        finally:
+            if gc_was:
+                gc.enable()
         torch.cuda.current_stream(env.device).wait_stream(stream)
         world.rng.cur = start_cur
 
-    def step(self, i: int = 0) -> StepResult:
-        """Replay the step reading actions[i]; returns its static outputs."""
+    def _replay(self, i: int) -> list:
         rng = self.env.world.rng
         key = (rng.cur, i)
         self._graphs[key].replay()
-        if self._rng_mode:
+        if self._rng_mode and self.steps_per_replay % 2:
             rng.flip()
         return self._results[key]
+
+    def step(self, i: int = 0) -> StepResult:
+        """Replay graph i; returns the outputs of its last step."""
+        return self._replay(i)[-1]
+
+    def rollout(self, i: int = 0) -> list:
+        """Replay graph i; returns the S StepResults of its steps, in order."""
+        return self._replay(i)
 
 
 def _make_world(scenario: Scenario, batch_size: int, rng, device) -> World:

@@ -269,6 +269,35 @@ def test_step_graph_equals_eager(cuda):
         assert a.rng.state()["state"]["counter"].tolist() == b.rng.state()["state"]["counter"].tolist()
 
 
+@pytest.mark.parametrize("S_", [2, 3])
+def test_multi_step_graph_equals_eager(cuda, S_):
+    """steps_per_replay=S: one replay runs S steps over actions[i], actions[i+1], ...
+    cyclically; every intermediate StepResult equals eager stepping, and the
+    Philox state (discovery draws every step) ends where eager leaves it,
+    for odd and even S."""
+    for name, ov in [("transport", {}), ("discovery", {"n_agents": 8})]:
+        a = env(name, B=300, cuda=cuda, seed=5, ov=ov, validate=False)
+        b = env(name, B=300, cuda=cuda, seed=5, ov=ov, validate=False)
+        A = len(a.agents)
+        g = torch.Generator(device=cuda)
+        g.manual_seed(3)
+        bufs = [torch.rand((A, 300, 2), device=cuda, generator=g) * 2 - 1 for _ in range(3)]
+        graph = b.step_graph(bufs, steps_per_replay=S_)
+        k = 0
+        for rep in range(4):
+            i = rep % 3
+            rs = graph.rollout(i)
+            assert len(rs) == S_
+            for s in range(S_):
+                ra = a.step(bufs[(i + s) % 3])
+                rb = rs[s]
+                for x, y in zip(ra.obs + ra.rewards + [ra.dones], rb.obs + rb.rewards + [rb.dones]):
+                    assert torch.equal(x, y)
+                k += 1
+        np.testing.assert_array_equal(state(a), state(b))
+        assert a.rng.state()["state"]["counter"].tolist() == b.rng.state()["state"]["counter"].tolist()
+
+
 def test_discrete_noise_and_fallback_paths_match_oracle_semantics(cuda):
     """Host-decoded forces (discrete actions) go through the same fused kernel
     with raw_forces; a world edit that breaks the kernel's pair template falls

@@ -30,8 +30,29 @@ def main() -> None:
     ap.add_argument("sizes", type=int, nargs="+")
     ap.add_argument("--steps", type=int, default=50)
     args = ap.parse_args()
-    scen, ov, _ = WORKLOADS[args.scenario]
     dev = torch.device("cuda:0")
+    if args.scenario == "probe":
+        # the timing floor of this harness: a graph of one 1-element kernel
+        x = torch.zeros(1, device=dev)
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s), torch.cuda.graph(g, stream=s):
+            x.add_(1.0)
+        torch.cuda.current_stream().wait_stream(s)
+        for _ in range(1000):
+            g.replay()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(200)]
+        torch.cuda.synchronize()
+        for a, b in ev:
+            a.record()
+            g.replay()
+            b.record()
+        torch.cuda.synchronize()
+        print(json.dumps({"probe": "1-element kernel graph", "kernel_ms": float(np.median([a.elapsed_time(b) for a, b in ev])),
+                          "ms_per_step": ev[0][0].elapsed_time(ev[-1][1]) / len(ev)}))
+        return
+    scen, ov, _ = WORKLOADS[args.scenario]
     hbm = peaks()["hbm_gbs"]
     for B in args.sizes:
         env = Env(create_scenario(scen, **ov), B, seed=0, device=dev, validate=False)
