@@ -1,5 +1,6 @@
 // ss_capi.cu — the extern "C" boundary (include/swarmsim_b200.h).
 #include <cstdio>
+#include <cstdlib>
 #include <new>
 
 #include "ss_geometry.cuh"
@@ -9,6 +10,11 @@ namespace ss {
 static thread_local std::string g_last_error;
 
 void set_error(const std::string& msg) { g_last_error = msg; }
+
+bool pdl_enabled() {
+  static const bool on = std::getenv("SS_NO_PDL") == nullptr;
+  return on;
+}
 
 int cuda_status(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return SS_OK;

@@ -32,6 +32,7 @@ SS_DEV V2 load_pos(const DevState& s, const SsEntityDesc& d, int64_t e) {
 
 __global__ void __launch_bounds__(32) k_generic_physics(const GenericArgs a) {
   extern __shared__ float sm[];
+  grid_dep_sync();
   if (a.guard && *a.guard) return;
   const int lane = threadIdx.x;
   const int64_t B = a.s.B;
@@ -137,7 +138,7 @@ int launch_generic(World& w, const SsBuffers* buf, const SsStepIO* io, const uin
     cudaFuncSetAttribute(k_generic_physics, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
   }
   const unsigned grid = (unsigned)((w.d.batch + 31) / 32);
-  k_generic_physics<<<grid, 32, shmem, st>>>(a);
+  launch_step(k_generic_physics, dim3(grid), dim3(32), shmem, st, a);
   return cuda_status(cudaGetLastError(), "generic world_step launch");
 }
 
@@ -199,6 +200,7 @@ struct CheckArgs {
 };
 
 __global__ void k_check_actions(const CheckArgs a) {
+  grid_dep_sync();
   const float* p = a.act[blockIdx.y];
   bool bad = false;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;
@@ -219,7 +221,7 @@ int launch_check_actions(int n_agents, int64_t B, const float* const* actions, i
   a.flag = flag;
   const int64_t want = (a.n + 255) / 256;
   const unsigned gx = (unsigned)(want < 1184 ? want : 1184);
-  k_check_actions<<<dim3(gx, n_agents), 256, 0, st>>>(a);
+  launch_step(k_check_actions, dim3(gx, n_agents), dim3(256), 0, st, a);
   return cuda_status(cudaGetLastError(), "action check launch");
 }
 

@@ -82,6 +82,39 @@ inline PhysK make_phys(const World& w) {
 // ---------------------------------------------------------------------------
 #define SS_DEV __device__ __forceinline__
 
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch.  Step kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization (launch_step), so the
+// next step's grid is launched while this one drains instead of after it.
+// Every such kernel starts with grid_dep_sync(): it waits until the previous
+// grid in the stream has completed with its memory visible (no data is
+// touched before), then releases its own dependents — they can only launch
+// once all of this grid's CTAs are resident, so they never take a slot this
+// grid still needs.  Without the attribute both instructions are no-ops.
+// ---------------------------------------------------------------------------
+SS_DEV void grid_dep_sync() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+bool pdl_enabled();   // SS_NO_PDL unset
+
+template <typename... KArgs, typename... Args>
+inline void launch_step(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                        Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // numpy clip(x, -u, u) with f32 bounds (env.py:97).
 SS_DEV float clip_sym(float x, float u) { return fminf(fmaxf(x, -u), u); }
 

@@ -24,6 +24,13 @@
 namespace ss {
 
 constexpr int kLargeWarps = 8;
+#ifndef SS_OBS_UNROLL
+#define SS_OBS_UNROLL 4
+#endif
+constexpr int kObsUnroll = SS_OBS_UNROLL;
+#ifndef SS_LARGE_MINB
+#define SS_LARGE_MINB 5   // resident CTAs (of 8 warps) per SM the register budget targets
+#endif
 constexpr int kLargeMaxAgents = 128;
 constexpr int kLargeMaxLandmarks = 128;
 
@@ -62,7 +69,7 @@ struct WarpSmem {
   float2* vel;     // [NA]
   float2* lm;      // [NL] landmark positions
   float* tmpl;     // template (16-byte aligned)
-  float* tmpl_shift;  // discovery: tmpl slots shifted by one (slot s holds slot s+1)
+  float* tmpl_shift;  // discovery: the contact bitmap (NA x u64) of agents_physics
   float* tmp;      // [2*NL] per-landmark scratch
   uint32_t* bits;  // [4] landmark flag words
 };
@@ -72,7 +79,7 @@ __host__ __device__ inline int round4(int n) { return (n + 3) & ~3; }
 // First region: discovery's float2 template [2 + NL + NA], or dispersion's
 // float template [4 + 3 NL] followed by its agent positions [NA] (float2).
 __host__ __device__ inline int tmpl_floats(int NA, int NL) {
-  const int disc = 2 * round4(2 * (2 + NL + NA));   // template + one-slot-shifted copy
+  const int disc = 2 * round4(2 * (2 + NL + NA));   // template + contact bitmap (2 NA floats fit)
   const int disp = round4(4 + 3 * NL) + 2 * NA;
   return round4(disc > disp ? disc : disp);
 }
@@ -108,7 +115,8 @@ SS_DEV WarpSmem carve(float* base, int NA, int NL, bool discovery) {
 // Leaves post-step positions in sm.pos (or `posbuf`) and velocities in sm.vel.
 template <int T, bool PAIRS>
 SS_DEV void agents_physics(const LargeArgs& a, float2* pos, float2* vel, int64_t e, float (&px)[T],
-                           float (&py)[T], float (&vx)[T], float (&vy)[T]) {
+                           float (&py)[T], float (&vx)[T], float (&vy)[T],
+                           unsigned long long* masks = nullptr) {
   const int lane = threadIdx.x & 31;
   const int64_t B = a.s.B;
 #pragma unroll
@@ -135,7 +143,57 @@ SS_DEV void agents_physics(const LargeArgs& a, float2* pos, float2* vel, int64_t
         if (a.ph.has_gravity) { fx[t] = fadd(fx[t], d.grav_x); fy[t] = fadd(fy[t], d.grav_y); }
       }
     }
-    if (PAIRS) {
+    if (PAIRS && masks != nullptr && a.NA <= 64) {
+      // Contact bitmap.  The squared distance is symmetric (a - b == -(b - a)
+      // and (-x)^2 == x^2 bitwise), so each unordered pair is tested once:
+      // lane l tests rows l and NA-1-l against their higher partners (NA-1
+      // tests on every lane) and records an active pair in both agents'
+      // 64-bit partner masks.  Each lane then walks its own agents' masks in
+      // increasing partner order — the reference's per-entity summation
+      // order, (j, k) subtractions for j < k before (k, j) additions — and
+      // evaluates the oriented exact contact only for those partners.
+      const int NA = a.NA;
+      for (int k = lane; k < NA; k += 32) masks[k] = 0ull;
+      __syncwarp();
+      if (lane < (NA + 1) / 2) {
+        const int r1 = lane, r2 = NA - 1 - lane, n1 = NA - 1 - lane;
+        const int nt = (r1 == r2) ? n1 : NA - 1;
+        const float2 p1 = pos[r1], p2 = pos[r2];
+#pragma unroll 4
+        for (int q = 0; q < nt; ++q) {
+          const bool first = q < n1;
+          const int k = first ? r1 : r2;
+          const int j = first ? r1 + 1 + q : r2 + 1 + (q - n1);
+          const float2 pk = first ? p1 : p2;
+          const float2 pj = pos[j];
+          if (sqnorm(fsub(pk.x, pj.x), fsub(pk.y, pj.y)) <= a.d2_act) {
+            atomicOr(masks + k, 1ull << j);
+            atomicOr(masks + j, 1ull << k);
+          }
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        const int k = lane + 32 * t;
+        if (k >= NA) continue;
+        unsigned long long m = masks[k];
+        while (m) {
+          const int j = __ffsll((long long)m) - 1;
+          m &= m - 1ull;
+          const float2 pj = pos[j];
+          const float sign = ((j + k) & 1) ? -1.0f : 1.0f;
+          float cx, cy;
+          if (j < k) {
+            contact_force(pj.x, pj.y, px[t], py[t], a.dmin, a.d2_act, sign, a.ph.ck, a.ph.k, cx, cy);
+            fx[t] = fsub(fx[t], cx); fy[t] = fsub(fy[t], cy);
+          } else {
+            contact_force(px[t], py[t], pj.x, pj.y, a.dmin, a.d2_act, sign, a.ph.ck, a.ph.k, cx, cy);
+            fx[t] = fadd(fx[t], cx); fy[t] = fadd(fy[t], cy);
+          }
+        }
+      }
+    } else if (PAIRS) {
       // The squared distance is symmetric ((-x)^2 == x^2 bitwise), so the
       // activity test runs once per (j, k) on pk - pj; the oriented, exact
       // contact (the reference's operand order) only in the rare active case.
@@ -201,9 +259,23 @@ struct ChunkWalk {
 // ---------------------------------------------------------------------------
 // discovery (scenarios/discovery.py)
 // ---------------------------------------------------------------------------
+// 16-byte chunk c of discovery observation row r (see k_discovery).
+SS_DEV float4 disc_chunk(const float2* t2, const WarpSmem& sm, int first_agent_slot, int r, int c) {
+  const int skip = first_agent_slot + r;
+  const int s0 = 2 * c, s1 = s0 + 1;
+  const float2 q0 = t2[s0 + (s0 >= skip)], q1 = t2[s1 + (s1 >= skip)];
+  const float2 pk = sm.pos[r];
+  if (c == 0) {
+    const float2 vk = sm.vel[r];
+    return make_float4(pk.x, pk.y, vk.x, vk.y);
+  }
+  return make_float4(fsub(q0.x, pk.x), fsub(q0.y, pk.y), fsub(q1.x, pk.x), fsub(q1.y, pk.y));
+}
+
 template <int T, int VEC>
-__global__ void __launch_bounds__(32 * kLargeWarps) k_discovery(const LargeArgs a) {
+__global__ void __launch_bounds__(32 * kLargeWarps, SS_LARGE_MINB) k_discovery(const LargeArgs a) {
   extern __shared__ __align__(16) float smem[];
+  grid_dep_sync();
   if (a.guard && *a.guard) return;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t B = a.s.B;
@@ -216,7 +288,12 @@ __global__ void __launch_bounds__(32 * kLargeWarps) k_discovery(const LargeArgs 
   const WarpSmem sm = carve(smem + wid * warp_floats(a.NA, a.NL), a.NA, a.NL, true);
   for (int i = lane; i < a.NL; i += 32) sm.lm[i] = a.s.stat[i * B + e];
   float px[T], py[T], vx[T], vy[T];
+#ifdef SS_NO_PAIR_BITMAP
   agents_physics<T, true>(a, sm.pos, sm.vel, e, px, py, vx, vy);
+#else
+  agents_physics<T, true>(a, sm.pos, sm.vel, e, px, py, vx, vy,
+                          reinterpret_cast<unsigned long long*>(sm.tmpl_shift));
+#endif
 
   int64_t steps = 0;
   if (a.mode & (SS_DO_COUNT | SS_DO_DONE)) {
@@ -304,48 +381,65 @@ __global__ void __launch_bounds__(32 * kLargeWarps) k_discovery(const LargeArgs 
     // row(k) = [x, y, vx, vy, (point_i - a_k)_i, (a_o - a_k)_{o != k}]
     // template slots: tmpl2[2 + i] = point_i, tmpl2[2 + NL + o] = a_o
     // Row k skips agent k's own slot: template slot s for s < 2 + NL + k,
-    // slot s + 1 beyond it.  tmpl_shift holds the template shifted by one
-    // slot, so every chunk is one 16-byte shared load from either copy
-    // (only the chunk straddling the skip mixes the two).
+    // slot s + 1 beyond it.
     const float2* t2 = reinterpret_cast<const float2*>(sm.tmpl);
-    const float2* t2s = reinterpret_cast<const float2*>(sm.tmpl_shift);
-    const int nslot = 2 + a.NL + a.NA;
-    for (int s = lane; s + 1 < nslot; s += 32) reinterpret_cast<float2*>(sm.tmpl_shift)[s] = t2[s + 1];
-    __syncwarp();
     const int first_agent_slot = 2 + a.NL;
-    const int slots = a.O >> 1;
-    const int nch = slots / (VEC / 2);          // chunks per row
-    const int total = a.NA * nch;
-    ChunkWalk w(lane, nch, a.obs + e * a.O, a.obs_stride);
-    for (int idx = lane; idx < total; idx += 32) {
-      const float2 pk = sm.pos[w.r];
-      const int skip = first_agent_slot + w.r;   // first slot served from the shifted copy
-      if (VEC == 4) {
-        const int s0 = 2 * w.c;
-        float4 v;
-        if (w.c == 0) {
-          const float2 vk = sm.vel[w.r];
-          v = make_float4(pk.x, pk.y, vk.x, vk.y);
-        } else if (s0 + 1 < skip || s0 >= skip) {
-          const float4 q = reinterpret_cast<const float4*>(s0 >= skip ? t2s : t2)[w.c];
-          v = make_float4(fsub(q.x, pk.x), fsub(q.y, pk.y), fsub(q.z, pk.x), fsub(q.w, pk.y));
-        } else {
-          const float2 q0 = t2[s0], q1 = t2s[s0 + 1];
-          v = make_float4(fsub(q0.x, pk.x), fsub(q0.y, pk.y), fsub(q1.x, pk.x), fsub(q1.y, pk.y));
+    if (VEC == 4) {
+      // all rows' 16-byte chunks as one flattened run, lane l taking l,
+      // l+32, ...; slot s of row k reads template slot s + (s >= 2+NL+k)
+      // (row k skips agent k's own slot); chunk 0 is [x, y, vx, vy]
+      const int nch = a.O >> 2;
+      const int total = a.NA * nch;
+      const int64_t stride4 = a.obs_stride >> 2;
+      if (nch >= 32) {
+        int r = 0, c = lane;                      // lane < 32 <= nch: row 0
+        float4* rowp = reinterpret_cast<float4*>(a.obs + e * a.O);
+        int idx = lane;
+        // kObsUnroll chunks per lane and round: all shared loads first, then
+        // the subtractions and streaming stores (latency overlap)
+        for (; idx + 32 * (kObsUnroll - 1) < total; idx += 32 * kObsUnroll) {
+          float4 v[kObsUnroll];
+          float4* dst[kObsUnroll];
+#pragma unroll
+          for (int u = 0; u < kObsUnroll; ++u) {
+            v[u] = disc_chunk(t2, sm, first_agent_slot, r, c);
+            dst[u] = rowp + c;
+            c += 32;
+            if (c >= nch) { c -= nch; ++r; rowp += stride4; }
+          }
+#pragma unroll
+          for (int u = 0; u < kObsUnroll; ++u) __stcs(dst[u], v[u]);
         }
-        __stcs(reinterpret_cast<float4*>(w.rowp) + w.c, v);
+        for (; idx < total; idx += 32) {
+          __stcs(rowp + c, disc_chunk(t2, sm, first_agent_slot, r, c));
+          c += 32;
+          if (c >= nch) { c -= nch; ++r; rowp += stride4; }
+        }
       } else {
+        for (int idx = lane; idx < total; idx += 32) {
+          const int r = idx / nch, c = idx - r * nch;
+          __stcs(reinterpret_cast<float4*>(a.obs + r * a.obs_stride + e * a.O) + c,
+                 disc_chunk(t2, sm, first_agent_slot, r, c));
+        }
+      }
+    } else {
+      const int slots = a.O >> 1;
+      const int total = a.NA * slots;
+      ChunkWalk w(lane, slots, a.obs + e * a.O, a.obs_stride);
+      for (int idx = lane; idx < total; idx += 32) {
+        const float2 pk = sm.pos[w.r];
+        const int skip = first_agent_slot + w.r;
         const int s = w.c;
         float2 v;
         if (s == 0) v = pk;
         else if (s == 1) v = sm.vel[w.r];
         else {
-          const float2 q = s >= skip ? t2s[s] : t2[s];
+          const float2 q = t2[s + (s >= skip)];
           v = make_float2(fsub(q.x, pk.x), fsub(q.y, pk.y));
         }
         __stcs(reinterpret_cast<float2*>(w.rowp) + w.c, v);
+        w.advance(slots, a.obs_stride);
       }
-      w.advance(nch, a.obs_stride);
     }
   }
 }
@@ -354,8 +448,9 @@ __global__ void __launch_bounds__(32 * kLargeWarps) k_discovery(const LargeArgs 
 // dispersion (scenarios/dispersion.py): agents non-collidable (no pairs).
 // ---------------------------------------------------------------------------
 template <int T, int VEC>
-__global__ void __launch_bounds__(32 * kLargeWarps) k_dispersion(const LargeArgs a) {
+__global__ void __launch_bounds__(32 * kLargeWarps, SS_LARGE_MINB) k_dispersion(const LargeArgs a) {
   extern __shared__ __align__(16) float smem[];
+  grid_dep_sync();
   if (a.guard && *a.guard) return;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t B = a.s.B;
@@ -520,7 +615,7 @@ int launch_large(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_
   do {                                                                                 \
     if (shmem > 48 * 1024)                                                             \
       cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem); \
-    K<<<grid, 32 * kLargeWarps, shmem, st>>>(a);                                       \
+    launch_step(K, dim3(grid), dim3(32 * kLargeWarps), shmem, st, a);                  \
   } while (0)
   if (w.d.scenario == SS_SCN_DISCOVERY) {
     if (v4) {

@@ -204,6 +204,7 @@ struct SpreadEnv {
 template <int NA>
 __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_simple_spread(const SmallArgs a) {
   extern __shared__ __align__(16) float smem[];
+  grid_dep_sync();
   if (a.guard && *a.guard) return;
   constexpr int O = SpreadEnv<NA>::O;
   const int64_t B = a.s.B;
@@ -285,6 +286,7 @@ template <int NA>
 __global__ void __launch_bounds__(kPipeTile) k_simple_spread_pipe(const SmallArgs a, int64_t ntiles) {
   extern __shared__ __align__(16) float smem_pipe[];
   PipeSmem<NA>& S = *reinterpret_cast<PipeSmem<NA>*>(smem_pipe);
+  grid_dep_sync();
   if (a.guard && *a.guard) return;
   constexpr int O = SpreadEnv<NA>::O;
   const int tid = threadIdx.x;
@@ -376,6 +378,7 @@ __global__ void __launch_bounds__(kPipeTile) k_simple_spread_pipe(const SmallArg
 template <int NA>
 __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_transport(const SmallArgs a) {
   extern __shared__ __align__(16) float smem[];
+  grid_dep_sync();
   if (a.guard && *a.guard) return;
   constexpr int O = 12;
   const int64_t B = a.s.B;
@@ -709,6 +712,7 @@ inline RayScreen make_screen(double r, double max_range) {
 template <int NA>
 __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_flocking(const SmallArgs a, const FlockLidarK lk) {
   extern __shared__ __align__(16) float smem_raw[];
+  grid_dep_sync();
   if (a.guard && *a.guard) return;
   const int NO = a.si[4];
   const int O = a.obs_dim;
@@ -898,6 +902,7 @@ template <int NA>
 __global__ void __launch_bounds__(32 * NA, (SS_FLOCK_WARPS / NA < 32 ? SS_FLOCK_WARPS / NA : 32))
     k_flocking_w(const SmallArgs a, const FlockLidarK lk) {
   extern __shared__ __align__(16) float smem_w[];
+  grid_dep_sync();
   if (a.guard && *a.guard) return;
   const int NO = a.si[4];
   const int O = a.obs_dim;
@@ -1154,13 +1159,13 @@ int launch_small(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_
       const int64_t rest = B - a.e_begin;
       if (rest <= 0) break;
       const unsigned g2 = (unsigned)((rest + kSmallThreads - 1) / kSmallThreads);
-#define SS_CASE(n) case n: k_simple_spread<n><<<g2, kSmallThreads, shmem, st>>>(a); break;
+#define SS_CASE(n) case n: launch_step(k_simple_spread<n>, dim3(g2), dim3(kSmallThreads), shmem, st, a); break;
       switch (NA) { SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) }
 #undef SS_CASE
       break;
     }
     case SS_SCN_TRANSPORT: {
-#define SS_CASE(n) case n: k_transport<n><<<grid, kSmallThreads, shmem, st>>>(a); break;
+#define SS_CASE(n) case n: launch_step(k_transport<n>, dim3(grid), dim3(kSmallThreads), shmem, st, a); break;
       switch (NA) { SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) }
 #undef SS_CASE
       break;
@@ -1208,7 +1213,7 @@ int launch_small(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_
     if (wshmem > 48 * 1024)                                                                 \
       cudaFuncSetAttribute(k_flocking_w<n>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
                            (int)wshmem);                                                    \
-    k_flocking_w<n><<<wgrid, 32 * n, wshmem, st>>>(a, lk);                                  \
+    launch_step(k_flocking_w<n>, dim3(wgrid), dim3(32 * n), wshmem, st, a, lk);                                     \
     break;
         switch (NA) { SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) }
 #undef SS_CASE
@@ -1222,7 +1227,7 @@ int launch_small(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_
     if (fshmem > 48 * 1024)                                                                 \
       cudaFuncSetAttribute(k_flocking<n>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
                            (int)fshmem);                                                    \
-    k_flocking<n><<<grid, kSmallThreads, fshmem, st>>>(a, lk);                              \
+    launch_step(k_flocking<n>, dim3(grid), dim3(kSmallThreads), fshmem, st, a, lk);                                \
     break;
       switch (NA) { SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) }
 #undef SS_CASE
