@@ -115,6 +115,44 @@ inline void launch_step(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t 
   cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
+// ---------------------------------------------------------------------------
+// Packed float32 pairs (sm_100 FADD2 / FMUL2): two independent IEEE
+// round-to-nearest float32 operations per instruction, no flush-to-zero — each
+// lane of the pair is bitwise the scalar __fadd_rn / __fsub_rn / __fmul_rn, so
+// they halve the instruction count of the elementwise x/y work without
+// touching parity.
+// ---------------------------------------------------------------------------
+SS_DEV float2 fsub2(float2 a, float2 b) {
+  float2 r;
+  asm("{.reg .b64 a, b, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "sub.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+SS_DEV float2 fadd2(float2 a, float2 b) {
+  float2 r;
+  asm("{.reg .b64 a, b, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "add.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+SS_DEV float2 fmul2(float2 a, float2 b) {
+  float2 r;
+  asm("{.reg .b64 a, b, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "mul.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+// (sqnorm of pair .x, sqnorm of pair .y) for dx = (dx0, dx1), dy = (dy0, dy1).
+// NEVER feed fmul2 into fadd2/fsub2: ptxas contracts mul.rn.f32x2 +
+// add.rn.f32x2 into FFMA2 even under -fmad=false (checked on nvcc 12.9), which
+// would round once instead of twice.  The sums stay scalar (__fadd_rn is
+// never contracted); tests/test_native_abi.py asserts the library holds no FFMA2.
+SS_DEV float2 sqnorm2(float2 dx, float2 dy) {
+  const float2 x2 = fmul2(dx, dx), y2 = fmul2(dy, dy);
+  return make_float2(__fadd_rn(x2.x, y2.x), __fadd_rn(x2.y, y2.y));
+}
+
 // numpy clip(x, -u, u) with f32 bounds (env.py:97).
 SS_DEV float clip_sym(float x, float u) { return fminf(fmaxf(x, -u), u); }
 

@@ -159,8 +159,22 @@ SS_DEV void agents_physics(const LargeArgs& a, float2* pos, float2* vel, int64_t
         const int r1 = lane, r2 = NA - 1 - lane, n1 = NA - 1 - lane;
         const int nt = (r1 == r2) ? n1 : NA - 1;
         const float2 p1 = pos[r1], p2 = pos[r2];
-#pragma unroll 4
-        for (int q = 0; q < nt; ++q) {
+        // tests q and q + 1 side by side in packed float32 pairs
+        int q = 0;
+#pragma unroll 2
+        for (; q + 1 < nt; q += 2) {
+          const bool fa = q < n1, fb = q + 1 < n1;
+          const int ka = fa ? r1 : r2, kb = fb ? r1 : r2;
+          const int ja = fa ? r1 + 1 + q : r2 + 1 + (q - n1);
+          const int jb = fb ? r1 + 2 + q : r2 + 2 + (q - n1);
+          const float2 pa = fa ? p1 : p2, pb = fb ? p1 : p2;
+          const float2 qa = pos[ja], qb = pos[jb];
+          const float2 d2 = sqnorm2(fsub2(make_float2(pa.x, pb.x), make_float2(qa.x, qb.x)),
+                                    fsub2(make_float2(pa.y, pb.y), make_float2(qa.y, qb.y)));
+          if (d2.x <= a.d2_act) { atomicOr(masks + ka, 1ull << ja); atomicOr(masks + ja, 1ull << ka); }
+          if (d2.y <= a.d2_act) { atomicOr(masks + kb, 1ull << jb); atomicOr(masks + jb, 1ull << kb); }
+        }
+        if (q < nt) {
           const bool first = q < n1;
           const int k = first ? r1 : r2;
           const int j = first ? r1 + 1 + q : r2 + 1 + (q - n1);
@@ -269,7 +283,8 @@ SS_DEV float4 disc_chunk(const float2* t2, const WarpSmem& sm, int first_agent_s
     const float2 vk = sm.vel[r];
     return make_float4(pk.x, pk.y, vk.x, vk.y);
   }
-  return make_float4(fsub(q0.x, pk.x), fsub(q0.y, pk.y), fsub(q1.x, pk.x), fsub(q1.y, pk.y));
+  const float2 d0 = fsub2(q0, pk), d1 = fsub2(q1, pk);
+  return make_float4(d0.x, d0.y, d1.x, d1.y);
 }
 
 template <int T, int VEC>
@@ -444,6 +459,25 @@ __global__ void __launch_bounds__(32 * kLargeWarps, SS_LARGE_MINB) k_discovery(c
   }
 }
 
+// 16-byte chunk c of dispersion observation row r: chunk c > 0 covers
+// template floats 4c..4c+3; element 4c+u belongs to item field (c - 1 + u) % 3:
+// 0 -> x (minus own x), 1 -> y, 2 -> eaten flag (minus +0: bitwise unchanged).
+SS_DEV float4 disp_chunk(const WarpSmem& sm, const float2* apos, int r, int c) {
+  const float2 pk = apos[r];
+  if (c == 0) {
+    const float2 vk = sm.vel[r];
+    return make_float4(pk.x, pk.y, vk.x, vk.y);
+  }
+  const int m = (c - 1) % 3;
+  const float4 t = reinterpret_cast<const float4*>(sm.tmpl)[c];
+  const float s0 = m == 0 ? pk.x : (m == 1 ? pk.y : 0.0f);
+  const float s1 = m == 0 ? pk.y : (m == 1 ? 0.0f : pk.x);
+  const float s2 = m == 0 ? 0.0f : (m == 1 ? pk.x : pk.y);
+  const float2 lo = fsub2(make_float2(t.x, t.y), make_float2(s0, s1));
+  const float2 hi = fsub2(make_float2(t.z, t.w), make_float2(s2, s0));
+  return make_float4(lo.x, lo.y, hi.x, hi.y);
+}
+
 // ---------------------------------------------------------------------------
 // dispersion (scenarios/dispersion.py): agents non-collidable (no pairs).
 // ---------------------------------------------------------------------------
@@ -471,14 +505,21 @@ __global__ void __launch_bounds__(32 * kLargeWarps, SS_LARGE_MINB) k_dispersion(
   // "reached" (any d <= eat_dist  <=>  min d2 <= bound) and the hunger term
   // (sqrt of the min).
   if (a.mode & (SS_DO_POST | SS_DO_REWARD)) {
-    for (int i = lane; i < a.NL; i += 32) {
-      const float2 f = sm.lm[i];
-      float best = __int_as_float(0x7f800000);
+    // food items i and i + 32 of a lane side by side in packed float32 pairs
+    for (int i = lane; i < a.NL; i += 64) {
+      const bool two = i + 32 < a.NL;
+      const float2 f0 = sm.lm[i], f1 = two ? sm.lm[i + 32] : f0;
+      const float2 fx = make_float2(f0.x, f1.x), fy = make_float2(f0.y, f1.y);
+      float b0 = __int_as_float(0x7f800000), b1 = b0;
+#pragma unroll 4
       for (int j = 0; j < a.NA; ++j) {
         const float2 p = apos[j];
-        best = fminf(best, sqnorm(fsub(p.x, f.x), fsub(p.y, f.y)));
+        const float2 d2 = sqnorm2(fsub2(make_float2(p.x, p.x), fx), fsub2(make_float2(p.y, p.y), fy));
+        b0 = fminf(b0, d2.x);
+        b1 = fminf(b1, d2.y);
       }
-      sm.tmp[i] = best;
+      sm.tmp[i] = b0;
+      if (two) sm.tmp[i + 32] = b1;
     }
   }
   if (lane < a.W) sm.bits[lane] = a.s.flags[lane * B + e];
@@ -539,26 +580,37 @@ __global__ void __launch_bounds__(32 * kLargeWarps, SS_LARGE_MINB) k_dispersion(
     __syncwarp();
     const int nch = a.O / VEC;
     const int total = a.NA * nch;
+    if (VEC == 4 && nch >= 32) {
+      // flattened (row, chunk) run as in k_discovery, kObsUnroll chunks per round
+      int r = 0, c = lane;
+      float4* rowp = reinterpret_cast<float4*>(a.obs + e * a.O);
+      const int64_t stride4 = a.obs_stride >> 2;
+      int idx = lane;
+      for (; idx + 32 * (kObsUnroll - 1) < total; idx += 32 * kObsUnroll) {
+        float4 v[kObsUnroll];
+        float4* dst[kObsUnroll];
+#pragma unroll
+        for (int u = 0; u < kObsUnroll; ++u) {
+          v[u] = disp_chunk(sm, apos, r, c);
+          dst[u] = rowp + c;
+          c += 32;
+          if (c >= nch) { c -= nch; ++r; rowp += stride4; }
+        }
+#pragma unroll
+        for (int u = 0; u < kObsUnroll; ++u) __stcs(dst[u], v[u]);
+      }
+      for (; idx < total; idx += 32) {
+        __stcs(rowp + c, disp_chunk(sm, apos, r, c));
+        c += 32;
+        if (c >= nch) { c -= nch; ++r; rowp += stride4; }
+      }
+      return;
+    }
     ChunkWalk w(lane, nch, a.obs + e * a.O, a.obs_stride);
     for (int idx = lane; idx < total; idx += 32) {
       const float2 pk = apos[w.r];
       if (VEC == 4) {
-        float4 v;
-        if (w.c == 0) {
-          const float2 vk = sm.vel[w.r];
-          v = make_float4(pk.x, pk.y, vk.x, vk.y);
-        } else {
-          // chunk c covers template floats 4c..4c+3; element 4c+u belongs to
-          // item field (c - 1 + u) % 3: 0 -> x (minus own x), 1 -> y, 2 -> flag.
-          // Subtracting +0 leaves the flag bitwise unchanged.
-          const int m = (w.c - 1) % 3;
-          const float4 t = reinterpret_cast<const float4*>(sm.tmpl)[w.c];
-          const float s0 = m == 0 ? pk.x : (m == 1 ? pk.y : 0.0f);
-          const float s1 = m == 0 ? pk.y : (m == 1 ? 0.0f : pk.x);
-          const float s2 = m == 0 ? 0.0f : (m == 1 ? pk.x : pk.y);
-          v = make_float4(fsub(t.x, s0), fsub(t.y, s1), fsub(t.z, s2), fsub(t.w, s0));
-        }
-        __stcs(reinterpret_cast<float4*>(w.rowp) + w.c, v);
+        __stcs(reinterpret_cast<float4*>(w.rowp) + w.c, disp_chunk(sm, apos, w.r, w.c));
       } else {
         const int j = w.c;
         float x;

@@ -77,3 +77,19 @@ def test_world_create_validates_descriptor_without_gpu():
     d.batch = 0
     with pytest.raises(ContractViolation, match="batch_size"):
         N.check(N.lib().ss_world_create(ctypes.byref(d), ctypes.byref(h)))
+
+
+def test_sass_has_no_packed_fused_multiply_add():
+    """The bit-exact contract forbids contracting a*b + c: ptxas fuses
+    mul.rn.f32x2 + add.rn.f32x2 into FFMA2 even under -fmad=false, so the
+    packed helpers (ss_internal.cuh) never chain them — checked on the SASS
+    of the built library (scalar FFMA appears only in the explicit fma of the
+    glibc expf / log1pf / sin-cos restatements)."""
+    import shutil
+
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not Path(tool).exists():
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([tool, "-sass", str(N.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "FMUL2" in sass or "FADD2" in sass          # the packed path is compiled in
+    assert "FFMA2" not in sass
