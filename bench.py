@@ -382,7 +382,10 @@ def run_b200(args, rank, world, local) -> None:
                          "traffic_source": "profiles/r01/ncu_traffic.json (ncu --set full, one launch)",
                          "bytes_per_env_step": bpe, "kernel_ms": ms_launch, "peak_source": pk["source"]},
             "e2e": {"value": e2e_value, "unit": "agent-steps/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
+                    "d2h_bytes_per_step": d2h,
+                    # the host link carries every step's actions in and obs / rewards /
+                    # dones out: achieved PCIe GB/s per GPU (one direction at a time)
+                    "link_gbs": (h2d + d2h) * E2E_K / e2e_sec / 1e9},
             "gpu_launches": K,
             "steps_per_replay": S,
             "episode_stats": {"mean_return_1step": episode["mean_return"], "envs": episode["envs"],

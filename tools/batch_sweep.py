@@ -2,9 +2,10 @@
 
     python tools/batch_sweep.py SCENARIO B1 B2 ... [--steps K]
 
-For each batch size: a fresh Env stepped by CUDA-graph replay of the fused
-step with device-resident random actions (two buffers cycled), 0.3 s clock
-soak, then K timed steps.  Prints one JSON line per size: per-launch median
+For each batch size: a fresh Env stepped by CUDA-graph replays of --spr
+consecutive fused steps with device-resident random actions (two buffers
+cycled), 0.3 s clock soak, then K timed steps.  `probe` instead times a
+graph of one 1-element kernel: the harness floor.  Prints one JSON line per size: per-launch median
 kernel time (CUDA events around each replay), ms per step over the whole
 timed loop, env-steps/s, agent-steps/s and the HBM roofline fraction
 (algorithmic bytes per env-step).
@@ -29,6 +30,7 @@ def main() -> None:
     ap.add_argument("scenario")
     ap.add_argument("sizes", type=int, nargs="+")
     ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--spr", type=int, default=10, help="steps per graph replay")
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     if args.scenario == "probe":
@@ -60,14 +62,15 @@ def main() -> None:
         O = env.observations()[0].shape[1]
         bpe = bytes_per_env_step(scen, A, len(env.world.entities) - A, O)
         acts = [torch.rand((A, B, 2), device=dev) * 2 - 1 for _ in range(2)]
-        g = env.step_graph(acts)
+        S = args.spr if A * B * (O * 4 + 4) * args.spr <= 4e9 else 1
+        g = env.step_graph(acts, steps_per_replay=S)
         t0, n = time.perf_counter(), 0
         while time.perf_counter() - t0 < 0.3:
             g.step(n % 2)
             n += 1
-            if n % 64 == 0:
+            if n % 16 == 0:
                 torch.cuda.synchronize()
-        K = args.steps
+        K = max(1, args.steps // S)
         s = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
         torch.cuda.synchronize()
         ends = []
@@ -79,10 +82,11 @@ def main() -> None:
             ends.append(e)
         s[K].record()
         torch.cuda.synchronize()
-        launch = float(np.median([s[k].elapsed_time(ends[k]) for k in range(K)]))
-        total = s[0].elapsed_time(s[K]) / K
+        launch = float(np.median([s[k].elapsed_time(ends[k]) for k in range(K)])) / S
+        total = s[0].elapsed_time(s[K]) / (K * S)
         rate = B / (total / 1e3)
-        print(json.dumps({"scenario": args.scenario, "envs": B, "kernel_ms": launch, "ms_per_step": total,
+        print(json.dumps({"scenario": args.scenario, "envs": B, "steps_per_replay": S, "kernel_ms": launch,
+                          "ms_per_step": total,
                           "env_steps_per_s": rate, "agent_steps_per_s": rate * A,
                           "bytes_per_env_step": bpe, "hbm_frac": bpe * B / (launch / 1e3) / 1e9 / hbm,
                           "working_set_mb": bpe * B / 1e6}), flush=True)

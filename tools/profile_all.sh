@@ -1,25 +1,33 @@
 #!/usr/bin/env bash
-# Profiling run for profiles/ (execute on the GPU box via gpurun, 1 GPU):
-#   1. the bench command plainly, then its ncu launch list (per-launch times)
-#   2. per workload: the step loop plainly, then one ncu --set full capture of
-#      the fused step kernel (ncu only after the same command exited 0).
+# Profiling runs for profiles/ (execute on the GPU box via gpurun, 1 GPU; one
+# ncu invocation per gpurun call):
+#   bash tools/profile_all.sh launches     bench plainly, then its ncu launch list
+#   bash tools/profile_all.sh SCENARIO     step loop plainly, then one ncu --set full
+#                                          capture of the fused kernel in steady state
+# Summaries land in gpurun_out/ (tools/ncu_summary.py); the .ncu-rep is deleted
+# to keep the merge-back small.
 set -u
 OUT=gpurun_out
 mkdir -p $OUT
-BENCH="python bench.py --steps 10 --warmup 3 --soak 0 --no-cpu"
-$BENCH > $OUT/plain_bench.log 2>&1 && \
-  ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-      --log-file $OUT/launches_simple_spread.csv $BENCH > $OUT/ncu_launches.log 2>&1
-declare -A KERN=([simple_spread]=k_simple_spread [transport]=k_transport [flocking]=k_flocking \
+what=${1:-launches}
+if [ "$what" = launches ]; then
+  BENCH="python bench.py --steps 10 --warmup 3 --soak 0 --no-cpu"
+  $BENCH > $OUT/plain_bench.log 2>&1 && \
+    ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+        --log-file $OUT/launches_simple_spread.csv $BENCH > $OUT/ncu_launches.log 2>&1
+  echo "launches: $?"
+  exit 0
+fi
+declare -A KERN=([simple_spread]=k_simple_spread [transport]=k_transport [flocking]=k_flocking_w \
                  [dispersion]=k_dispersion [discovery]=k_discovery)
-for s in simple_spread transport flocking dispersion discovery; do
-  CMD="python tools/step_loop.py $s 0 3"
-  $CMD > $OUT/plain_$s.log 2>&1 && \
-    ncu --set full --clock-control none --import-source on -k regex:${KERN[$s]} -s 1 -c 1 \
-        -o $OUT/full_$s $CMD > $OUT/ncu_full_$s.log 2>&1
-  echo "$s: $?"
-done
-# keep gpurun_out small: summaries only
-for s in simple_spread transport flocking dispersion discovery; do
-  [ -f $OUT/full_$s.ncu-rep ] && python tools/ncu_summary.py $OUT/full_$s.ncu-rep $OUT/full_$s && rm -f $OUT/full_$s.ncu-rep
-done
+# launches skipped before the capture: steady state (flocking's agents
+# gather at the beacon after ~1k steps; the others settle within tens)
+declare -A PRE=([simple_spread]=20 [transport]=200 [flocking]=1500 [dispersion]=20 [discovery]=50)
+s=$what
+CMD="python tools/step_loop.py $s 0 $((${PRE[$s]} + 2))"
+$CMD > $OUT/plain_$s.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:${KERN[$s]} -s ${PRE[$s]} -c 1 \
+      -o $OUT/full_$s $CMD > $OUT/ncu_full_$s.log 2>&1
+echo "$s: $?"
+[ -f $OUT/full_$s.ncu-rep ] && python tools/ncu_summary.py $OUT/full_$s.ncu-rep $OUT/full_$s && rm -f $OUT/full_$s.ncu-rep
+exit 0
