@@ -543,13 +543,27 @@ __global__ void __launch_bounds__(32 * kLargeWarps, SS_LARGE_MINB) k_dispersion(
     fresh = a.s.aux[e];
   }
   if (a.mode & SS_DO_REWARD) {   // dispersion.py:68-76, float64 hunger in item order
+    // the per-item terms (sqrt, cast) in parallel, then lane 0 adds them in
+    // item order (the float64 sum is order-sensitive); the terms overwrite
+    // the min-d2 scratch: NL doubles exactly fill its 2 NL floats
+    float d2v[kLargeMaxLandmarks / 32];
+#pragma unroll
+    for (int w = 0; w < kLargeMaxLandmarks / 32; ++w) {
+      const int i = lane + 32 * w;
+      d2v[w] = i < a.NL ? sm.tmp[i] : 0.0f;
+    }
+    __syncwarp();
+    double* term = reinterpret_cast<double*>(sm.tmp);
+#pragma unroll
+    for (int w = 0; w < kLargeMaxLandmarks / 32; ++w) {
+      const int i = lane + 32 * w;
+      if (i < a.NL) term[i] = ((sm.bits[w] >> lane) & 1u) ? 0.0 : (double)fsqrt(d2v[w]);
+    }
+    __syncwarp();
     float r = 0.0f;
     if (lane == 0) {
       double hunger = 0.0;
-      for (int i = 0; i < a.NL; ++i) {
-        const bool ate = (sm.bits[i >> 5] >> (i & 31)) & 1u;
-        hunger = dadd_rn(hunger, ate ? 0.0 : (double)fsqrt(sm.tmp[i]));
-      }
+      for (int i = 0; i < a.NL; ++i) hunger = dadd_rn(hunger, term[i]);
       r = (float)dsub_rn((double)fresh, dmul_rn(0.05, hunger));
     }
     r = __shfl_sync(0xffffffffu, r, 0);
