@@ -69,12 +69,12 @@ def integrate(entity: Entity, force: Vec2, torque, params: PhysParams) -> None:
         st.rot = st.rot + w * dt
 
 
-def _validate_action(agent: Agent, action: AgentAction, B: int) -> None:
-    """dynamics.py:103-120."""
+def _validate_action(agent: Agent, action: AgentAction, B: int, check_nan: bool = True) -> None:
+    """dynamics.py:103-120 (check_nan=False: Env(validate=False), no host sync)."""
     if action.force.batch_size != B:
         raise ContractViolation(
             f"action for '{agent.name}' has batch size {action.force.batch_size}, world has {B}")
-    if bool(torch.isnan(action.force.x).any() | torch.isnan(action.force.y).any()):
+    if check_nan and bool(torch.isnan(action.force.x).any() | torch.isnan(action.force.y).any()):
         raise ContractViolation(f"action for '{agent.name}' contains NaN")
     if action.comm is not None:
         if agent.silent:

@@ -74,12 +74,16 @@ def _to_device(raw, device) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(arr)).to(device, non_blocking=True)
 
 
-def decode_action(raw, spec: ActionSpec, agent: Agent, rng: SeededRng) -> AgentAction:
-    """Raw policy output -> AgentAction (env.py:71-145), on the agent's device."""
+def decode_action(raw, spec: ActionSpec, agent: Agent, rng: SeededRng, check: bool = True) -> AgentAction:
+    """Raw policy output -> AgentAction (env.py:71-145), on the agent's device.
+
+    check=False (Env(validate=False)) skips the NaN scan, the one host sync of
+    the continuous branch, so the decode can be captured in a CUDA graph.
+    """
     world = agent.state._world
     B, dev = world.batch_size, world.device
     t = _to_device(raw, dev)
-    if t.is_floating_point() and bool(torch.isnan(t).any()):
+    if check and t.is_floating_point() and bool(torch.isnan(t).any()):
         raise ContractViolation(f"action for '{agent.name}' contains NaN")
     if spec.mode == "continuous":
         if t.ndim == 1 and spec.comm_dim == 0 and tuple(t.shape) == (2,) and B == 1:
@@ -292,14 +296,14 @@ class Env:
         forces = []
         # scripts see the pre-step state and run in agent order, before any
         # physics (dynamics.py:136-138); a script replaces any raw action
-        decoded = [None if raw is None else decode_action(raw, spec, agent, self.rng)
+        decoded = [None if raw is None else decode_action(raw, spec, agent, self.rng, self.validate)
                    for raw, agent, spec in zip(raw_actions, self.agents, self.action_specs)]
         for act, agent in zip(decoded, self.agents):
             if agent.action_script is not None:
                 act = agent.action_script(agent, self.world)
             from .dynamics import _validate_action
 
-            _validate_action(agent, act, self.batch_size)
+            _validate_action(agent, act, self.batch_size, self.validate)
             agent.action = act
             if not agent.silent and act.comm is not None:
                 self.world.comm[agent.name] = act.comm
@@ -386,9 +390,13 @@ _BASE_INFO = Scenario.info
 class StepGraph:
     """Env.step as CUDA-graph replays — the launch-overhead-free stepping mode.
 
-    For built-in scenarios: each action buffer in `actions` (one or more
-    (A, B, 2) float32 device tensors, read in place at every replay) gets a
-    captured graph; step(i) replays graph i.  With steps_per_replay=S > 1 a
+    Each action buffer in `actions` (one or more (A, B, 2) float32 device
+    tensors, read in place at every replay) gets a captured graph; step(i)
+    replays graph i.  Built-in scenarios capture their fused launch; any
+    other scenario captures the generic path (ss_world_step + its torch
+    hooks) — scripted agents keep running their script, and a scenario that
+    syncs with the host or draws from the Env stream inside step is refused
+    (ContractViolation).  With steps_per_replay=S > 1 a
     graph holds S consecutive fused steps reading actions[i], actions[i+1],
     ... (cyclically) — an open-loop rollout whose S StepResults live in
     distinct graph-owned buffers (rollout(i)), so the GPU runs the steps back
@@ -400,8 +408,6 @@ class StepGraph:
     """
 
     def __init__(self, env: Env, actions, steps_per_replay: int = 1):
-        if not env.fused:
-            raise ContractViolation("StepGraph needs a built-in (fused) scenario")
         acts = [actions] if isinstance(actions, torch.Tensor) else list(actions)
         A, B = len(env.agents), env.batch_size
         S = int(steps_per_replay)
@@ -411,17 +417,28 @@ class StepGraph:
             if (t.device != env.device or t.dtype != torch.float32 or tuple(t.shape) != (A, B, 2)
                     or not t.is_contiguous()):
                 raise ContractViolation(f"StepGraph actions must be contiguous float32 ({A}, {B}, 2) on {env.device}")
-        if (env._needs_host_decode([0] * A) or any(s.comm_dim for s in env.action_specs)
-                or env._any_obs_noise):
-            raise ContractViolation("StepGraph covers continuous, noiseless, unscripted, silent agents")
+        if env.action_mode != "continuous" or any(s.comm_dim for s in env.action_specs) or env._any_obs_noise \
+                or any(a.action_noise_std > 0.0 for a in env.agents):
+            raise ContractViolation("StepGraph covers continuous, noiseless, silent agents")
+        if env.fused and env._needs_host_decode([0] * A):
+            raise ContractViolation("StepGraph on a built-in scenario covers unscripted agents")
         self.env = env
         self.actions = acts
         self.steps_per_replay = S
-        self._rng_mode = bool(env.scenario.advances_rng_per_step)
+        self._generic = not env.fused
         sc, world = env.scenario, env.world
+        self._rng_mode = bool(getattr(sc, "advances_rng_per_step", False))
         world.ensure_device_rng()
-        sc.native_handle(world)           # build the descriptor outside capture
-        sc.physics_fused(world)
+        if self._generic:
+            # generic worlds: physics through ss_world_step plus the scenario's
+            # torch hooks; they must not sync with the host or draw from the
+            # Env stream inside step (checked: a draw raises during capture)
+            from .dynamics import physics_world
+
+            physics_world(world)
+        else:
+            sc.native_handle(world)           # build the descriptor outside capture
+            sc.physics_fused(world)
         start_cur = world.rng.cur
         self._graphs: dict = {}
         self._results: dict = {}
@@ -433,23 +450,45 @@ class StepGraph:
         gc.collect()
         gc.disable()
         try:
-            for cur in ((0, 1) if self._rng_mode else (start_cur,)):
-                for i in range(len(acts)):
-                    world.rng.cur = cur       # each captured step flips it in rng mode
-                    g = torch.cuda.CUDAGraph()
-                    results = []
-                    with torch.cuda.stream(stream), torch.cuda.graph(g, stream=stream):
-                        for k in range(S):
-                            act = acts[(i + k) % len(acts)]
-                            base, stride = act.data_ptr(), B * 8
-                            results.append(env._capture_step([base + a * stride for a in range(A)], act))
-                    self._graphs[(cur, i)] = g
-                    self._results[(cur, i)] = results
+            self._capture_all(env, acts, A, B, S, start_cur, stream)
+        except RuntimeError as ex:
+            raise ContractViolation(f"step of '{type(sc).__name__}' is not capturable: {ex}") from ex
         finally:
             if gc_was:
                 gc.enable()
+            world.rng.capture_guard = False
         torch.cuda.current_stream(env.device).wait_stream(stream)
         world.rng.cur = start_cur
+
+    def _capture_all(self, env, acts, A, B, S, start_cur, stream) -> None:
+        world = env.world
+        for cur in ((0, 1) if self._rng_mode else (start_cur,)):
+            for i in range(len(acts)):
+                world.rng.cur = cur       # each captured step flips it in rng mode
+                g = torch.cuda.CUDAGraph()
+                results = []
+                with torch.cuda.stream(stream), torch.cuda.graph(g, stream=stream):
+                    for k in range(S):
+                        act = acts[(i + k) % len(acts)]
+                        if self._generic:
+                            results.append(self._capture_generic(act))
+                            continue
+                        base, stride = act.data_ptr(), B * 8
+                        results.append(env._capture_step([base + a * stride for a in range(A)], act))
+                self._graphs[(cur, i)] = g
+                self._results[(cur, i)] = results
+
+    def _capture_generic(self, act) -> StepResult:
+        env = self.env
+        saved, rng = env.validate, env.world.rng
+        env.validate = False
+        rng.capture_guard = True
+        try:
+            return env._step_generic([None if a.action_script is not None else act[n]
+                                      for n, a in enumerate(env.agents)])
+        finally:
+            env.validate = saved
+            rng.capture_guard = False
 
     def _replay(self, i: int) -> list:
         rng = self.env.world.rng
