@@ -593,7 +593,11 @@ SS_DEV uint32_t ray_window(float fx, float fy, const RayFan& fan, const RayScree
   if (!(f2 <= s.reach2)) return 0u;
   const float q = __fsub_rn(f2, __fmul_rn(s.rr, s.rr));
   if (!(q > 1e-6f)) return fan.all;
+#ifdef SS_TEST_SHRINK_FAN   // deliberately broken screen: tests must catch it
+  const float w = 0.97f * __fmul_rn(__fmul_rn(s.rr, rsqrtf(q)), fan.inv_step);
+#else
   const float w = __fmaf_rn(__fmul_rn(__fmul_rn(s.rr, rsqrtf(q)), fan.inv_step), 1.001f, 0.01f);
+#endif
   if (!(w < fan.quarter)) return fan.all;
   float v = __fmul_rn(__fsub_rn(fast_atan2(-fy, -fx), fan.start), fan.inv_step);
   v = __fsub_rn(v, __fmul_rn(fan.period, floorf(__fdividef(v, fan.period))));

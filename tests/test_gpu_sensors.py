@@ -86,3 +86,56 @@ def test_lidar_semantics(cuda):
     inside.add(S.Entity("b", S.Box(1.0, 0.5)))
     d = S.cast_ray(e2.state.pos, torch.tensor([0.0], dtype=torch.float64), inside, 5.0, exclude="e")
     assert abs(float(d[0]) - 0.5) < 1e-6                                        # inside a box: exit wall
+
+
+def test_fused_lidar_screen_adversarial(cuda):
+    """The fused flocking Lidar screens rays by angle (k_flocking_w) before the
+    exact float64 test.  Place circles on the screen's edges — tangent to a
+    ray at ±0..2e-4 of the radius, a hit at max_range ± eps, an emitter on or
+    just inside a rim — and require the observation (lidar columns included)
+    to equal the oracle's reference scan bit-for-bit."""
+    ov = {"n_agents": 5, "n_obstacles": 3, "lidar_rays": 12}
+    B = 8192
+    e = S.Env(S.create_scenario("flocking", **ov), B, seed=11, device=cuda)
+    o = O.OracleEnv("flocking", B, seed=11, **ov)
+    rng = np.random.default_rng(5)
+    st = e.world.state_array().cpu().numpy()
+    E = st.shape[0]
+    st[:, 0:2, :] = rng.uniform(-1.2, 1.2, (E, 2, B)).astype(np.float32)
+    st[:, 2:, :] = 0.0
+    r_rock, r_agent = 0.1, float(e.agents[0].shape.radius)
+    eps_set = [0.0, 1e-7, -1e-7, 1e-6, -1e-6, 1e-5, -1e-5, 5e-5, -5e-5, 1e-4, -1e-4, 2e-4, -2e-4]
+    for b in range(B):
+        em = int(rng.integers(5))
+        origin = st[em, 0:2, b].astype(np.float64)
+        m = int(rng.integers(12))
+        ang = 2 * np.pi * m / 12
+        d = np.array([np.cos(ang), np.sin(ang)])
+        nrm = np.array([-d[1], d[0]])
+        eps = eps_set[b % len(eps_set)]
+        kind = b % 4
+        if kind == 0:      # rock tangent to ray m of emitter em
+            c = origin + rng.uniform(0.05, 1.1) * d + rng.choice([-1, 1]) * (r_rock + eps) * nrm
+            st[5 + 1 + int(rng.integers(3)), 0:2, b] = c
+        elif kind == 1:    # agent tangent
+            other = (em + 1 + int(rng.integers(4))) % 5
+            c = origin + rng.uniform(0.05, 1.1) * d + rng.choice([-1, 1]) * (r_agent + eps) * nrm
+            st[other, 0:2, b] = c
+        elif kind == 2:    # hit at max_range +- eps along the ray
+            st[5 + 1 + int(rng.integers(3)), 0:2, b] = origin + (1.0 + r_rock + eps) * d
+        else:              # emitter on / just inside / just outside a rock's rim
+            st[5 + 1 + int(rng.integers(3)), 0:2, b] = origin + (r_rock + eps) * d
+    st = st.astype(np.float32)
+    e.world.load_state_array(torch.from_numpy(st).to(cuda))
+    got = [x.cpu().numpy() for x in e.observations()]
+    ws = o.ws
+    for k in range(E):
+        ws.px[k][:], ws.py[k][:] = st[k, 0], st[k, 1]
+        ws.vx[k][:], ws.vy[k][:] = st[k, 2], st[k, 3]
+        ws.rot[k][:], ws.w[k][:] = st[k, 4], st[k, 5]
+    want = o.task.obs(ws)
+    for a in range(5):
+        np.testing.assert_array_equal(got[a], want[a], err_msg=f"agent {a}")
+    # the edge cases really exercise the screen: some tangent rays hit, some miss
+    lid = np.concatenate([g[:, -12:] for g in got])
+    assert (lid < 1.0).any() and (lid == 1.0).any()
