@@ -637,7 +637,7 @@ constexpr int kLidarQueue = 64;    // (lane, target, ray) tests staged per warp 
 // Warp-collective: every lane of the warp must call it.
 template <int NA>
 SS_DEV void lidar_fan_warp(bool active, int i, int lane, int NO, float mex, float mey,
-                           const float4* sag, const float2* sst, const FlockLidarK& lk,
+                           const float2* spos, const float2* sst, const FlockLidarK& lk,
                            const double2* sdird, uint32_t* best, int P, uint32_t* queue, int n_rays) {
   constexpr int NT = NA - 1 + kFlockMaxRocks;
   uint32_t mk[NT];
@@ -648,7 +648,7 @@ SS_DEV void lidar_fan_warp(bool active, int i, int lane, int NO, float mex, floa
     if (active && (t < NA - 1 || t - (NA - 1) < NO)) {
       float qx, qy;
       if (t < NA - 1) {
-        const float4 q = sag[(t < i ? t : t + 1) * 32 + lane];
+        const float2 q = spos[(t < i ? t : t + 1) * 32 + lane];
         qx = q.x; qy = q.y;
       } else {
         const float2 q = sst[(t - (NA - 1) + 1) * 32 + lane];
@@ -686,10 +686,10 @@ SS_DEV void lidar_fan_warp(bool active, int i, int lane, int NO, float mex, floa
     for (int k = lane; k < nq; k += 32) {
       const uint32_t w = queue[k];
       const int sl = (int)(w & 31u), t = (int)((w >> 5) & 15u), r = (int)(w >> 9);
-      const float4 org = sag[i * 32 + sl];
+      const float2 org = spos[i * 32 + sl];
       double cx, cy, r2;
       if (t < NA - 1) {
-        const float4 q = sag[(t < i ? t : t + 1) * 32 + sl];
+        const float2 q = spos[(t < i ? t : t + 1) * 32 + sl];
         cx = q.x; cy = q.y; r2 = lk.r2_agent;
       } else {
         const float2 q = sst[(t - (NA - 1) + 1) * 32 + sl];
@@ -917,12 +917,15 @@ __global__ void __launch_bounds__(32 * NA, (SS_FLOCK_WARPS / NA < 32 ? SS_FLOCK_
   const int64_t e = e0 + lane;
   const bool valid = e < B;
   const int nvalid = (int)min((int64_t)32, B - e0);
-  // shared memory: [dirs: n_rays double2][agents: NA x 32 float4][queue: NA x kLidarQueue u32]
+  // shared memory: [dirs: n_rays double2][agents: NA x 32 float4 pre-step]
+  //                [agents: NA x 32 float2 post-step positions][queue: NA x kLidarQueue u32]
   //                [dirs: n_rays(+1) float2][static: (1+NO) x 32 float2][rows: NA warps x 32 x P]
-  // (the lidar minima are accumulated in the rows' lidar columns)
+  // (pre / post copies: one barrier between physics and the rest; the lidar
+  // minima are accumulated in the rows' lidar columns)
   double2* sdird = reinterpret_cast<double2*>(smem_w);
   float4* sag = reinterpret_cast<float4*>(sdird + a.n_rays);
-  uint32_t* squeue = reinterpret_cast<uint32_t*>(sag + NA * 32);
+  float2* spos = reinterpret_cast<float2*>(sag + NA * 32);
+  uint32_t* squeue = reinterpret_cast<uint32_t*>(spos + NA * 32);
   float2* sdir = reinterpret_cast<float2*>(squeue + NA * kLidarQueue);
   float2* sst = reinterpret_cast<float2*>(sdir + ((a.n_rays + 1) & ~1));
   float* srow = reinterpret_cast<float*>(sst + (1 + NO) * 32) + i * 32 * P;
@@ -975,9 +978,8 @@ __global__ void __launch_bounds__(32 * NA, (SS_FLOCK_WARPS / NA < 32 ? SS_FLOCK_
     integrate_lin(me.x, me.y, me.z, me.w, fx, fy, a.ph.keep, d.inv_m_dt, a.ph.dt, d.max_speed);
     a.s.dyn[i * B + e] = me;
   }
-  __syncthreads();                       // all partners read their pre-step positions
-  if (valid) sag[i * 32 + lane] = me;
-  __syncthreads();
+  if (valid) spos[i * 32 + lane] = make_float2(me.x, me.y);
+  __syncthreads();                       // post-step positions of every agent staged
   if (valid && (a.mode & SS_DO_COUNT)) { steps += 1; if (i == 0) a.s.step_count[e] = steps; }
   const float2 beacon = valid ? sst[lane] : make_float2(0.f, 0.f);
   if (valid && (a.mode & SS_DO_REWARD)) {
@@ -987,7 +989,7 @@ __global__ void __launch_bounds__(32 * NA, (SS_FLOCK_WARPS / NA < 32 ? SS_FLOCK_
 #pragma unroll
     for (int o = 0; o < NA; ++o) {
       if (o == i) continue;
-      const float4 q = sag[o * 32 + lane];
+      const float2 q = spos[o * 32 + lane];
       ca = fadd(ca, sqnorm(fsub(me.x, q.x), fsub(me.y, q.y)) <= thr2_aa ? 1.0f : 0.0f);
     }
     for (int r = 0; r < NO; ++r) {
@@ -1010,7 +1012,7 @@ __global__ void __launch_bounds__(32 * NA, (SS_FLOCK_WARPS / NA < 32 ? SS_FLOCK_
 #pragma unroll
       for (int o = 0; o < NA; ++o) {
         if (o == i) continue;
-        const float4 q = sag[o * 32 + lane];
+        const float2 q = spos[o * 32 + lane];
         row[c] = fsub(q.x, me.x); row[c + 1] = fsub(q.y, me.y); c += 2;
       }
     }
@@ -1025,7 +1027,7 @@ __global__ void __launch_bounds__(32 * NA, (SS_FLOCK_WARPS / NA < 32 ? SS_FLOCK_
       const float range_f = (float)a.lidar_range;
       if (lk.fan_ok) {
         // warp-collective: all lanes, including invalid / rotated ones
-        lidar_fan_warp<NA>(fan, i, lane, NO, me.x, me.y, sag, sst, lk, sdird, wbest, P, squeue + i * kLidarQueue,
+        lidar_fan_warp<NA>(fan, i, lane, NO, me.x, me.y, spos, sst, lk, sdird, wbest, P, squeue + i * kLidarQueue,
                            a.n_rays);
         if (fan)
           for (int m = 0; m < a.n_rays; ++m)
@@ -1035,7 +1037,7 @@ __global__ void __launch_bounds__(32 * NA, (SS_FLOCK_WARPS / NA < 32 ? SS_FLOCK_
 #pragma unroll
         for (int o = 0; o < NA; ++o) {
           if (o == i) continue;
-          const float4 q = sag[o * 32 + lane];
+          const float2 q = spos[o * 32 + lane];
           const uint32_t mk = ray_mask(me.x - q.x, me.y - q.y, sdir, a.n_rays, lk.agent);
           ray_hits_f(mk, ox, oy, sdird, (double)q.x, (double)q.y, lk.r2_agent, best, stride);
         }
@@ -1055,7 +1057,7 @@ __global__ void __launch_bounds__(32 * NA, (SS_FLOCK_WARPS / NA < 32 ? SS_FLOCK_
           double b = __longlong_as_double(0x7ff0000000000000LL);
           for (int o = 0; o < NA; ++o) {
             if (o == i) continue;
-            const float4 q = sag[o * 32 + lane];
+            const float2 q = spos[o * 32 + lane];
             b = fmin(b, ray_circle(ox, oy, dx, dy, (double)q.x, (double)q.y, lk.r2_agent));
           }
           for (int r = 0; r < NO; ++r) {
@@ -1072,7 +1074,7 @@ __global__ void __launch_bounds__(32 * NA, (SS_FLOCK_WARPS / NA < 32 ? SS_FLOCK_
 
 inline size_t flocking_w_smem(int NA, int NO, int n_rays, int O) {
   return (size_t)n_rays * sizeof(double2) + (size_t)NA * 32 * sizeof(float4) +
-         (size_t)NA * kLidarQueue * sizeof(uint32_t) +
+         (size_t)NA * 32 * sizeof(float2) + (size_t)NA * kLidarQueue * sizeof(uint32_t) +
          (size_t)((n_rays + 1) & ~1) * sizeof(float2) + (size_t)(1 + NO) * 32 * sizeof(float2) +
          (size_t)NA * 32 * (O | 1) * sizeof(float);
 }

@@ -200,9 +200,21 @@ def test_full_size_sampled_envs_match_oracle(cuda, name, B):
         np.testing.assert_array_equal(torch.stack(r.rewards).cpu().numpy()[:, idx], np.stack(rew))
 
 
-def test_bulk_copy_pipeline_matches_oracle(cuda):
-    """The opt-in cp.async.bulk pipeline (SS_PIPE=1, read once per process)
-    runs in a subprocess and must match the oracle bit-for-bit."""
+VARIANTS = [
+    ("SS_PIPE", "simple_spread", {}, 1000),                 # cp.async.bulk pipeline
+    ("SS_FLOCK_THREAD_PER_ENV", "flocking", {"n_agents": 5, "n_obstacles": 3, "lidar_rays": 12}, 300),
+    ("SS_LIDAR_NO_FAN", "flocking", {"n_agents": 5, "n_obstacles": 3, "lidar_rays": 12}, 300),
+    ("SS_NO_PDL", "transport", {}, 777),                    # plain launches
+]
+
+
+@pytest.mark.parametrize("var,name,ov,B", VARIANTS, ids=[v[0] for v in VARIANTS])
+def test_kernel_variants_match_oracle(cuda, var, name, ov, B):
+    """Every opt-in kernel variant (selected by an environment variable read
+    once per process) runs in a subprocess and must match the oracle
+    bit-for-bit: the bulk-copy pipeline, the thread-per-env flocking kernel,
+    the per-ray Lidar screen, launches without programmatic dependency."""
+    import os
     import subprocess
     import sys
 
@@ -211,22 +223,20 @@ import sys; sys.path[:0] = [%r, %r]
 import numpy as np, torch
 import golden_util as G, paper_2207_03530_b200 as S
 from oracle import swarm_oracle as O
-B = 1000
-e = S.Env(S.create_scenario("simple_spread"), B, seed=5, device="cuda", validate=False)
-o = O.OracleEnv("simple_spread", B, seed=5)
-for plan in G.pregen_actions(3, B, 12, 6):
+name, ov, B = %r, %r, %d
+e = S.Env(S.create_scenario(name, **ov), B, seed=5, device="cuda", validate=False)
+o = O.OracleEnv(name, B, seed=5, **ov)
+for plan in G.pregen_actions(len(e.agents), B, 12, 6):
     r = e.step(torch.from_numpy(np.stack(plan)).cuda())
     obs, rew, done = o.step(plan)
     for x, y in zip(r.obs, obs): np.testing.assert_array_equal(x.cpu().numpy(), y)
     np.testing.assert_array_equal(torch.stack(r.rewards).cpu().numpy(), np.stack(rew))
     np.testing.assert_array_equal(r.dones.cpu().numpy(), done)
-print("PIPE_OK")
-""" % (str(G.GOLDEN.parents[1]), str(G.GOLDEN.parent))
-    import os
-
-    res = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, SS_PIPE="1"),
+print("VARIANT_OK")
+""" % (str(G.GOLDEN.parents[1]), str(G.GOLDEN.parent), name, ov, B)
+    res = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **{var: "1"}),
                          capture_output=True, text=True, timeout=300)
-    assert "PIPE_OK" in res.stdout, res.stdout + res.stderr
+    assert "VARIANT_OK" in res.stdout, res.stdout + res.stderr
 
 
 def test_sharded_run_equals_single_run(cuda):
