@@ -375,12 +375,15 @@ __global__ void __launch_bounds__(kPipeTile) k_simple_spread_pipe(const SmallArg
 // sc[1] = half width, sc[2] = f32(success_dist); the doubles are passed via
 // si-packed bits: see make_small_args.
 // ---------------------------------------------------------------------------
-template <int NA>
+// REV = 1: reverse_transport (catalog scenarios/reverse_transport.py): the
+// same world (agents inside a hollow crate), observation
+// [x, y, vx, vy, crate - self, crate vel, goal - crate] (O = 10).
+template <int NA, int REV>
 __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_transport(const SmallArgs a) {
   extern __shared__ __align__(16) float smem[];
   grid_dep_sync();
   if (a.guard && *a.guard) return;
-  constexpr int O = 12;
+  constexpr int O = REV ? 10 : 12;
   const int64_t B = a.s.B;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = e < B;
@@ -471,9 +474,14 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_transport(cons
       if (valid) {
         row[0] = px[i]; row[1] = py[i]; row[2] = vx[i]; row[3] = vy[i];
         row[4] = fsub(px[NA], px[i]); row[5] = fsub(py[NA], py[i]);
-        row[6] = fsub(gx, px[i]); row[7] = fsub(gy, py[i]);
-        row[8] = fsub(px[NA], gx); row[9] = fsub(py[NA], gy);
-        row[10] = vx[NA]; row[11] = vy[NA];
+        if (REV) {
+          row[6] = vx[NA]; row[7] = vy[NA];
+          row[8] = fsub(gx, px[NA]); row[9] = fsub(gy, py[NA]);
+        } else {
+          row[6] = fsub(gx, px[i]); row[7] = fsub(gy, py[i]);
+          row[8] = fsub(px[NA], gx); row[9] = fsub(py[NA], gy);
+          row[10] = vx[NA]; row[11] = vy[NA];
+        }
       }
       if (nvalid > 0) warp_flush(a.obs + i * a.obs_stride + e0 * O, nvalid, O, sbuf);
     }
@@ -1171,7 +1179,11 @@ int launch_small(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_
       break;
     }
     case SS_SCN_TRANSPORT: {
-#define SS_CASE(n) case n: launch_step(k_transport<n>, dim3(grid), dim3(kSmallThreads), shmem, st, a); break;
+#define SS_CASE(n)                                                                         \
+  case n:                                                                                  \
+    if (w.d.si[1]) launch_step(k_transport<n, 1>, dim3(grid), dim3(kSmallThreads), shmem, st, a); \
+    else launch_step(k_transport<n, 0>, dim3(grid), dim3(kSmallThreads), shmem, st, a);           \
+    break;
       switch (NA) { SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) }
 #undef SS_CASE
       break;

@@ -440,9 +440,13 @@ class Passage(Scenario):
 
 
 # ---------------------------------------------------------------------------
-@register("reverse_transport")
 class ReverseTransport(Scenario):
-    """Agents trapped inside a hollow crate drive it to a goal."""
+    """Agents trapped inside a hollow crate drive it to a goal.
+
+    The registered "reverse_transport" is the fused version
+    (scenarios/reverse_transport.py: k_transport's reverse layout); this torch
+    implementation supplies its world, reset and heuristic, and stays the
+    generic-path restatement of the reference hooks."""
 
     max_steps = 250
 
