@@ -489,6 +489,97 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_transport(cons
 }
 
 // ---------------------------------------------------------------------------
+// dropout (catalog scenarios/dropout.py): NA non-collidable agents (dyn
+// 0..NA-1), goal marker (stat row 0); no pairs.  Reward (shared):
+// float64(any agent within reach) - energy_coeff * spent, spent = the float64
+// sum over agents, in order, of fx*fx then fy*fy (float32 squares of the
+// decoded actions, promoted); done = reached.  spent is kept in flag words 0
+// and 1 (double bits) so a reward-only launch sees the last step's value.
+// sc[3] = squared bound of f32(reach); sd[0] = energy_coeff.
+// Observation: [x, y, vx, vy, goal - self, (other - self)].
+// ---------------------------------------------------------------------------
+template <int NA>
+__global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_dropout(const SmallArgs a) {
+  extern __shared__ __align__(16) float smem[];
+  grid_dep_sync();
+  if (a.guard && *a.guard) return;
+  constexpr int O = 4 + 2 * NA;
+  const int64_t B = a.s.B;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = e < B;
+  float px[NA], py[NA], vx[NA], vy[NA];
+  float2 u[NA];
+  float gx = 0.f, gy = 0.f;
+  int64_t steps = 0;
+  uint32_t lo = 0u, hi = 0u;
+  if (valid) {
+    // every global load of the step issued up front
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      const float4 q = a.s.dyn[i * B + e];
+      px[i] = q.x; py[i] = q.y; vx[i] = q.z; vy[i] = q.w;
+    }
+    const float2 g = a.s.stat[e];
+    gx = g.x; gy = g.y;
+    if (a.mode & SS_DO_PHYSICS) {
+#pragma unroll
+      for (int i = 0; i < NA; ++i) u[i] = a.act[i][e];
+    } else if (a.mode & SS_DO_REWARD) {
+      lo = a.s.flags[e];
+      hi = a.s.flags[B + e];
+    }
+    if (a.mode & (SS_DO_COUNT | SS_DO_DONE)) steps = a.s.step_count[e];
+  }
+  double spent = __hiloint2double((int)hi, (int)lo);
+  if (valid && (a.mode & SS_DO_PHYSICS)) {
+    spent = 0.0;
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      const SsEntityDesc& d = a.ents[i];
+      float fx = decode_axis(u[i].x, d, a.raw_forces), fy = decode_axis(u[i].y, d, a.raw_forces);
+      spent = dadd_rn(dadd_rn(spent, (double)fmul(fx, fx)), (double)fmul(fy, fy));
+      if (a.ph.has_gravity) { fx = fadd(fx, d.grav_x); fy = fadd(fy, d.grav_y); }
+      integrate_lin(px[i], py[i], vx[i], vy[i], fx, fy, a.ph.keep, d.inv_m_dt, a.ph.dt, d.max_speed);
+      a.s.dyn[i * B + e] = make_float4(px[i], py[i], vx[i], vy[i]);
+    }
+    a.s.flags[e] = (uint32_t)__double2loint(spent);
+    a.s.flags[B + e] = (uint32_t)__double2hiint(spent);
+  }
+  if (valid && (a.mode & SS_DO_COUNT)) { steps += 1; a.s.step_count[e] = steps; }
+  bool reached = false;
+  if (valid) {
+#pragma unroll
+    for (int i = 0; i < NA; ++i) reached |= sqnorm(fsub(px[i], gx), fsub(py[i], gy)) <= a.sc[3];
+  }
+  if (valid && (a.mode & SS_DO_REWARD)) {
+    const float r = (float)dsub_rn(reached ? 1.0 : 0.0, dmul_rn(a.sd[0], spent));
+#pragma unroll
+    for (int i = 0; i < NA; ++i) __stcs(a.rew + i * B + e, r);
+  }
+  if (valid && (a.mode & SS_DO_DONE)) a.done[e] = (uint8_t)(reached | (steps >= a.ph.max_steps));
+  if (a.mode & SS_DO_OBS) {
+    float* sbuf = smem + (threadIdx.x >> 5) * (32 * O);
+    float* row = sbuf + (threadIdx.x & 31) * O;
+    const int64_t e0 = e - (threadIdx.x & 31);
+    const int nvalid = (int)min((int64_t)32, B - e0);
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      if (valid) {
+        row[0] = px[i]; row[1] = py[i]; row[2] = vx[i]; row[3] = vy[i];
+        row[4] = fsub(gx, px[i]); row[5] = fsub(gy, py[i]);
+        int c = 6;
+#pragma unroll
+        for (int o = 0; o < NA; ++o) {
+          if (o == i) continue;
+          row[c++] = fsub(px[o], px[i]); row[c++] = fsub(py[o], py[i]);
+        }
+      }
+      if (nvalid > 0) warp_flush(a.obs + i * a.obs_stride + e0 * O, nvalid, O, sbuf);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // flocking (scenarios/flocking.py): NA agents (dyn 0..NA-1), beacon marker
 // (entity NA, stat row 0), NO rocks (entity NA+1+r, stat row 1+r, immovable).
 // Pairs, lexicographic: for i: agents j>i, then rocks.  Optional Lidar
@@ -1184,6 +1275,12 @@ int launch_small(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_
     if (w.d.si[1]) launch_step(k_transport<n, 1>, dim3(grid), dim3(kSmallThreads), shmem, st, a); \
     else launch_step(k_transport<n, 0>, dim3(grid), dim3(kSmallThreads), shmem, st, a);           \
     break;
+      switch (NA) { SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) }
+#undef SS_CASE
+      break;
+    }
+    case SS_SCN_DROPOUT: {
+#define SS_CASE(n) case n: launch_step(k_dropout<n>, dim3(grid), dim3(kSmallThreads), shmem, st, a); break;
       switch (NA) { SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) }
 #undef SS_CASE
       break;

@@ -501,9 +501,12 @@ class ReverseTransport(Scenario):
 
 
 # ---------------------------------------------------------------------------
-@register("dropout")
 class Dropout(Scenario):
-    """Any one agent reaching the goal scores; every agent pays for effort."""
+    """Any one agent reaching the goal scores; every agent pays for effort.
+
+    The registered "dropout" is the fused version (scenarios/dropout.py:
+    k_dropout); this torch implementation supplies its world and heuristic
+    and stays the generic-path restatement of the reference hooks."""
 
     max_steps = 200
 

@@ -113,3 +113,22 @@ def test_generic_step_graph_equals_eager(cuda, name):
                 assert torch.equal(x, y)
     assert torch.equal(a.world.state_array(), b.world.state_array())
     assert torch.equal(a.step_count, b.step_count)
+
+
+@pytest.mark.parametrize("name", ["simple_spread", "transport", "flocking", "dispersion", "discovery",
+                                  "reverse_transport", "dropout"])
+def test_fused_hooks_equal_step_outputs(cuda, name):
+    """The reference's Scenario hooks on a fused world (single-phase kernel
+    launches: reward, done, observation) reproduce what Env.step returned —
+    dropout's reward reads the last step's energy from the flag words,
+    dispersion's the fresh bites from aux."""
+    env = S.Env(S.create_scenario(name), 96, seed=4, device=cuda)
+    rng = S.SeededRng(8)
+    for _ in range(3):
+        res = env.step([rng.uniform(-a.u_range, a.u_range, (96, 2)) for a in env.agents])
+    sc, w = env.scenario, env.world
+    for i, agent in enumerate(env.agents):
+        assert torch.equal(sc.reward(agent, w), res.rewards[i])
+        assert torch.equal(sc.observation(agent, w), res.obs[i])
+    horizon = env.step_count >= env.max_steps
+    assert torch.equal(sc.done(w) | horizon, res.dones)
