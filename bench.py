@@ -1,12 +1,14 @@
 """Benchmark: batched env-step throughput on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--scenario simple_spread]
-                    [--envs B_PER_GPU] [--impl b200|reference]
+                    [--envs B_PER_GPU] [--strong] [--impl b200|reference]
 
 One JSON line on rank 0.  A "step" is one Env.step of the whole batch on
 every GPU (weak scaling: B envs per GPU; rank r holds the global env range
 [r*B, (r+1)*B) of one N*B-env batch, so the sharded run is the 1-GPU run of
-N*B envs, random stream included).  Inputs are device-resident synthetic
+N*B envs, random stream included).  --strong keeps the batch global (e.g.
+dispersion / discovery: 262144 envs sharded over 1/2/4/8 GPUs, BASELINE
+config 5) and reports "scaling": "strong".  Inputs are device-resident synthetic
 uniform actions; the working set (341 B/env at 1M envs = 341 MB) exceeds the
 126 MB L2, so no flush is needed between steps.
 
@@ -259,9 +261,18 @@ def run_b200(args, rank, world, local) -> None:
 
     dev = torch.device("cuda", local)
     scen, ov, default_b = WORKLOADS[args.scenario]
-    B = args.envs or default_b
+    if args.strong:
+        # strong scaling: the workload's batch is the GLOBAL batch, sharded
+        # over the ranks with the global random-stream layout (parallel.py)
+        from paper_2207_03530_b200.parallel import shard_range
+
+        Bg = args.envs or default_b
+        off, B = shard_range(rank, world, Bg)
+    else:
+        B = args.envs or default_b
+        off, Bg = rank * B, world * B
     env = Env(create_scenario(scen, **ov), B, seed=0, device=dev, validate=False,
-              env_offset=rank * B, global_batch=world * B)
+              env_offset=off, global_batch=Bg)
     A = len(env.agents)
     O = len(env.observations()[0][0])
     n_other = len(env.world.entities) - A
@@ -312,7 +323,7 @@ def run_b200(args, rank, world, local) -> None:
     # per-step device time of the fused kernel: each replay's events / S
     per_launch = sorted(s.elapsed_time(e) / S for s, e in zip(starts, ends))
     ms_launch = float(np.median(per_launch))
-    env_steps = world * B * K
+    env_steps = Bg * K
     value = env_steps * A / (ms_total / 1000.0)
     achieved = bpe * B / (ms_launch / 1e3) / 1e9
 
@@ -321,7 +332,7 @@ def run_b200(args, rank, world, local) -> None:
     # guard), host actions in, observations / rewards / dones back to host
     del graph
     env_e2e = Env(create_scenario(scen, **ov), B, seed=0, device=dev, validate=True,
-                  env_offset=rank * B, global_batch=world * B)
+                  env_offset=off, global_batch=Bg)
     E2E_K = max(3, min(K, 10))
     host_acts = [[torch.from_numpy(np.random.default_rng(7 + k).uniform(-1, 1, (B, 2)).astype(np.float32)).pin_memory()
                   for _ in range(A)] for k in range(E2E_K + 1)]
@@ -343,7 +354,7 @@ def run_b200(args, rank, world, local) -> None:
     for k in range(1, E2E_K + 1):
         e2e_step(k)
     e2e_sec = max_over_ranks(time.perf_counter() - t0e, world, dev)
-    e2e_value = world * B * A * E2E_K / e2e_sec
+    e2e_value = Bg * A * E2E_K / e2e_sec
     h2d = A * B * 8
     d2h = A * B * O * 4 + A * B * 4 + B
 
@@ -370,10 +381,12 @@ def run_b200(args, rank, world, local) -> None:
             "metric": "agent-steps/sec", "value": value, "unit": "agent-steps/s",
             "env_steps_per_s": env_steps / (ms_total / 1000.0),
             "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms_total / K,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "strong" if args.strong else "weak", "vs_baseline": None,
+            "dtype": "f32",
             "data": "synthetic uniform actions in [-1,1]; env state from the scenario's reset distribution",
-            "config": {"workload": f"{scen} {ov}, {B} envs per GPU", "scenario": scen,
-                       "envs_per_gpu": B, "global_envs": world * B, "agents": A, "obs_dim": O,
+            "config": {"workload": (f"{scen} {ov}, {Bg} envs sharded over {world} GPU(s)" if args.strong
+                                    else f"{scen} {ov}, {B} envs per GPU"), "scenario": scen,
+                       "envs_per_gpu": B, "global_envs": Bg, "agents": A, "obs_dim": O,
                        "l2": "working set > L2 (no flush needed)" if bpe * B > 126e6 else "L2-resident",
                        "stepping": f"Env.step_graph(steps_per_replay={S}): CUDA-graph replays of {S} consecutive "
                                    f"fused steps, {pool} action buffer(s) cycled; e2e uses eager Env.step(validate=True)"},
@@ -405,6 +418,8 @@ def main() -> None:
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--scenario", choices=sorted(WORKLOADS), default="simple_spread")
     ap.add_argument("--envs", type=int, default=0, help="envs per GPU (default: the workload's)")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: --envs / the workload's batch is the global batch, sharded over ranks")
     ap.add_argument("--cpu-envs", type=int, default=1_000_000)
     ap.add_argument("--cpu-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true")
