@@ -15,7 +15,9 @@ uniform actions; the working set (341 B/env at 1M envs = 341 MB) exceeds the
   value  — agent-steps/s over all GPUs, kernel path (actions resident in HBM),
            CUDA-event timed, max over ranks.
   e2e    — the same metric through the public API with host buffers: pinned
-           host actions copied in and obs/rewards/dones copied out every step.
+           host actions copied in and obs/rewards/dones copied out every step
+           (e2e.obs_on_device: the same with observations left in HBM for a
+           GPU policy, only rewards / dones copied out).
   roofline — the fused step kernel: algorithmic bytes / launch time vs the
            measured HBM copy bandwidth (MEASURED_PEAKS.json).
   cpu_baseline — the reference algorithm (oracle/swarm_oracle.py, a numpy
@@ -358,6 +360,20 @@ def run_b200(args, rank, world, local) -> None:
     h2d = A * B * 8
     d2h = A * B * O * 4 + A * B * 4 + B
 
+    # the same loop for a policy that runs on the GPU: observations stay in
+    # HBM, only rewards / dones (the logged metric) come back to the host
+    def e2e_metric_step(k):
+        res = env_e2e.step(host_acts[k])
+        rew_h.copy_(torch.stack(res.rewards), non_blocking=True)
+        done_h.copy_(res.dones, non_blocking=True)
+        torch.cuda.synchronize(dev)
+
+    barrier(world, dev)
+    t0m = time.perf_counter()
+    for k in range(1, E2E_K + 1):
+        e2e_metric_step(k)
+    metric_sec = max_over_ranks(time.perf_counter() - t0m, world, dev)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cb = min(B, args.cpu_envs)
@@ -398,7 +414,9 @@ def run_b200(args, rank, world, local) -> None:
                     "d2h_bytes_per_step": d2h,
                     # the host link carries every step's actions in and obs / rewards /
                     # dones out: achieved PCIe GB/s per GPU (one direction at a time)
-                    "link_gbs": (h2d + d2h) * E2E_K / e2e_sec / 1e9},
+                    "link_gbs": (h2d + d2h) * E2E_K / e2e_sec / 1e9,
+                    "obs_on_device": {"value": Bg * A * E2E_K / metric_sec, "h2d_bytes_per_step": h2d,
+                                      "d2h_bytes_per_step": A * B * 4 + B}},
             "gpu_launches": K,
             "steps_per_replay": S,
             "episode_stats": {"mean_return_1step": episode["mean_return"], "envs": episode["envs"],
