@@ -19,7 +19,8 @@ ABI_VERSION = 1
 RNG_WORDS = 12
 
 SS_SPHERE, SS_BOX, SS_LINE = 0, 1, 2
-SCN_PHYSICS_ONLY, SCN_SIMPLE_SPREAD, SCN_TRANSPORT, SCN_FLOCKING, SCN_DISPERSION, SCN_DISCOVERY, SCN_DROPOUT = range(7)
+(SCN_PHYSICS_ONLY, SCN_SIMPLE_SPREAD, SCN_TRANSPORT, SCN_FLOCKING, SCN_DISPERSION, SCN_DISCOVERY, SCN_DROPOUT,
+ SCN_WHEEL) = range(8)
 
 DO_PHYSICS, DO_POST, DO_COUNT, DO_REWARD, DO_DONE, DO_OBS = 1, 2, 4, 8, 16, 32
 MODE_STEP = 63

@@ -580,6 +580,57 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_dropout(const 
 }
 
 // ---------------------------------------------------------------------------
+// wheel (catalog scenarios/wheel.py): NA agents (dyn 0..NA-1) and a pinned
+// rotatable rod (entity NA, stat row 0).  Physics (sphere-line contacts and
+// the rod's torque) is world_step's (k_generic_physics, launched first);
+// this kernel does the rest of the step: count, reward -|w - target| (float32,
+// shared), horizon done, observation
+// [x, y, vx, vy, rod - self, cos(rot), sin(rot), w, target] with numpy's
+// float32 cos/sin.  sc[0] = f32(target_spin).
+// ---------------------------------------------------------------------------
+template <int NA>
+__global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_wheel(const SmallArgs a) {
+  extern __shared__ __align__(16) float smem[];
+  grid_dep_sync();
+  if (a.guard && *a.guard) return;
+  constexpr int O = 10;
+  const int64_t B = a.s.B;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = e < B;
+  int64_t steps = 0;
+  float2 rod = make_float2(0.f, 0.f), rw = rod;
+  if (valid) {
+    rod = a.s.stat[e];
+    rw = a.s.rot[NA * B + e];
+    if (a.mode & (SS_DO_COUNT | SS_DO_DONE)) steps = a.s.step_count[e];
+  }
+  if (valid && (a.mode & SS_DO_COUNT)) { steps += 1; a.s.step_count[e] = steps; }
+  if (valid && (a.mode & SS_DO_REWARD)) {
+    const float r = -fabsf(fsub(rw.y, a.sc[0]));
+#pragma unroll
+    for (int i = 0; i < NA; ++i) __stcs(a.rew + i * B + e, r);
+  }
+  if (valid && (a.mode & SS_DO_DONE)) a.done[e] = (uint8_t)(steps >= a.ph.max_steps);
+  if (a.mode & SS_DO_OBS) {
+    float* sbuf = smem + (threadIdx.x >> 5) * (32 * O);
+    float* row = sbuf + (threadIdx.x & 31) * O;
+    const int64_t e0 = e - (threadIdx.x & 31);
+    const int nvalid = (int)min((int64_t)32, B - e0);
+    const float c = valid ? np_cosf(rw.x) : 0.f, sn = valid ? np_sinf(rw.x) : 0.f;
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      if (valid) {
+        const float4 q = a.s.dyn[i * B + e];
+        row[0] = q.x; row[1] = q.y; row[2] = q.z; row[3] = q.w;
+        row[4] = fsub(rod.x, q.x); row[5] = fsub(rod.y, q.y);
+        row[6] = c; row[7] = sn; row[8] = rw.y; row[9] = a.sc[0];
+      }
+      if (nvalid > 0) warp_flush(a.obs + i * a.obs_stride + e0 * O, nvalid, O, sbuf);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // flocking (scenarios/flocking.py): NA agents (dyn 0..NA-1), beacon marker
 // (entity NA, stat row 0), NO rocks (entity NA+1+r, stat row 1+r, immovable).
 // Pairs, lexicographic: for i: agents j>i, then rocks.  Optional Lidar
@@ -1275,6 +1326,16 @@ int launch_small(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_
     if (w.d.si[1]) launch_step(k_transport<n, 1>, dim3(grid), dim3(kSmallThreads), shmem, st, a); \
     else launch_step(k_transport<n, 0>, dim3(grid), dim3(kSmallThreads), shmem, st, a);           \
     break;
+      switch (NA) { SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) }
+#undef SS_CASE
+      break;
+    }
+    case SS_SCN_WHEEL: {
+      if (a.mode & SS_DO_PHYSICS) {
+        set_error("wheel: physics runs through ss_world_step (generic kernel)");
+        return SS_ERR_CONTRACT;
+      }
+#define SS_CASE(n) case n: launch_step(k_wheel<n>, dim3(grid), dim3(kSmallThreads), shmem, st, a); break;
       switch (NA) { SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) }
 #undef SS_CASE
       break;

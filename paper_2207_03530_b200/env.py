@@ -437,8 +437,11 @@ class StepGraph:
 
             physics_world(world)
         else:
-            sc.native_handle(world)           # build the descriptor outside capture
-            sc.physics_fused(world)
+            sc.native_handle(world)           # build the descriptors outside capture
+            if not sc.physics_fused(world):
+                from .dynamics import physics_world
+
+                physics_world(world)          # world_step's generic kernel runs first
         start_cur = world.rng.cur
         self._graphs: dict = {}
         self._results: dict = {}

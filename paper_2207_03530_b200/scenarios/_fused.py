@@ -181,6 +181,32 @@ class FusedScenario(Scenario):
         world.rng.flip()
 
 
+class HostReset:
+    """Mixin for fused scenarios whose reset program runs on the host: the
+    reference's own reset code (`_reference.reset_world_at`, drawing from the
+    Env's Philox stream), one env at a time, ascending, for masked resets."""
+
+    _reference: type = None
+
+    def reset_ops(self, world):
+        return []
+
+    def reset_world_at(self, world: World, env_index: int | None = None) -> None:
+        self._reference.reset_world_at(self, world, env_index)
+
+    def reset_world_masked(self, world: World, mask: torch.Tensor, mask_base=None, mask_total=None) -> None:
+        if mask_base is not None:
+            from ..errors import ContractViolation
+
+            raise ContractViolation(f"{type(self).__name__} resets on the host: no sharded masked reset")
+        for i in torch.nonzero(mask).flatten().tolist():
+            self.reset_world_at(world, i)
+            world.step_count[i] = 0
+
+    def heuristic_action(self, agent_index: int, obs):
+        return self._reference.heuristic_action(self, agent_index, obs)
+
+
 class _Flag:
     """Cache entry with a close() so World._drop_native can clear it."""
 

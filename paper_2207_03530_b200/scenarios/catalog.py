@@ -53,9 +53,12 @@ def _np(obs):
 
 
 # ---------------------------------------------------------------------------
-@register("wheel")
 class Wheel(Scenario):
-    """Agents push the tips of a pinned rod to hold a target spin."""
+    """Agents push the tips of a pinned rod to hold a target spin.
+
+    The registered "wheel" is scenarios/wheel.py (world_step + k_wheel); this
+    torch implementation supplies its world, reset and heuristic and stays the
+    generic-path restatement of the reference hooks."""
 
     max_steps = 200
 

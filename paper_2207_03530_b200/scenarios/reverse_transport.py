@@ -12,18 +12,17 @@ Env's Philox stream, one env at a time for masked resets.
 """
 from __future__ import annotations
 
-import torch
-
 from ..core import World
-from ..errors import ContractViolation
 from . import register
+from ._fused import HostReset
 from .catalog import ReverseTransport as _Reference
 from .transport import Transport
 
 
 @register("reverse_transport")
-class ReverseTransport(Transport):
+class ReverseTransport(HostReset, Transport):
     max_steps = 250
+    _reference = _Reference
 
     def __init__(self, n_agents: int = 4, crate_size: float = 0.6, crate_mass: float = 3.0,
                  success_dist: float = 0.1):
@@ -34,25 +33,9 @@ class ReverseTransport(Transport):
     def make_world(self, batch_size: int, rng) -> World:
         return _Reference.make_world(self, batch_size, rng)
 
-    def reset_ops(self, world):
-        return []            # resets run on the host (reset_world_at)
-
     def obs_dim(self, world):
         return 10
 
     def fill_constants(self, world, d):
         super().fill_constants(world, d)
         d.si[1] = 1          # reverse observation layout
-
-    def reset_world_at(self, world: World, env_index: int | None = None) -> None:
-        _Reference.reset_world_at(self, world, env_index)
-
-    def reset_world_masked(self, world: World, mask: torch.Tensor, mask_base=None, mask_total=None) -> None:
-        if mask_base is not None:
-            raise ContractViolation("reverse_transport resets on the host: no sharded masked reset")
-        for i in torch.nonzero(mask).flatten().tolist():
-            self.reset_world_at(world, i)
-            world.step_count[i] = 0
-
-    def heuristic_action(self, agent_index: int, obs):
-        return _Reference.heuristic_action(self, agent_index, obs)
