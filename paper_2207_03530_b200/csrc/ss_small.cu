@@ -631,6 +631,64 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_wheel(const Sm
 }
 
 // ---------------------------------------------------------------------------
+// give_way (catalog scenarios/give_way.py): agents 0, 1 (dyn rows 0, 1),
+// goals 0, 1 (stat rows 0, 1), six walls.  Physics (sphere-line contacts) is
+// world_step's; this kernel: count, reward for agent k
+// f32(-float64(gap_k) + 5.0 * float64(gap_k < f32(0.15))), done = both gaps
+// < f32(0.15), observation [x, y, vx, vy, goal_k - self, other - self, other
+// vel, f32(alcove_x - float64(x)), f32(alcove_y - float64(y))].
+// sc[0] = f32(0.15); sd[0], sd[1] = alcove (python doubles).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_give_way(const SmallArgs a) {
+  extern __shared__ __align__(16) float smem[];
+  grid_dep_sync();
+  if (a.guard && *a.guard) return;
+  constexpr int O = 12;
+  const int64_t B = a.s.B;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = e < B;
+  float4 ag[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+  float2 goal[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+  int64_t steps = 0;
+  if (valid) {
+    ag[0] = a.s.dyn[e]; ag[1] = a.s.dyn[B + e];
+    goal[0] = a.s.stat[e]; goal[1] = a.s.stat[B + e];
+    if (a.mode & (SS_DO_COUNT | SS_DO_DONE)) steps = a.s.step_count[e];
+  }
+  if (valid && (a.mode & SS_DO_COUNT)) { steps += 1; a.s.step_count[e] = steps; }
+  const float thr = a.sc[0];
+  float gap[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) gap[k] = norm2(fsub(ag[k].x, goal[k].x), fsub(ag[k].y, goal[k].y));
+  if (valid && (a.mode & SS_DO_REWARD)) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      __stcs(a.rew + k * B + e, (float)dadd_rn(-(double)gap[k], gap[k] < thr ? 5.0 : 0.0));
+  }
+  if (valid && (a.mode & SS_DO_DONE))
+    a.done[e] = (uint8_t)(((gap[0] < thr) & (gap[1] < thr)) | (steps >= a.ph.max_steps));
+  if (a.mode & SS_DO_OBS) {
+    float* sbuf = smem + (threadIdx.x >> 5) * (32 * O);
+    float* row = sbuf + (threadIdx.x & 31) * O;
+    const int64_t e0 = e - (threadIdx.x & 31);
+    const int nvalid = (int)min((int64_t)32, B - e0);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      if (valid) {
+        const float4 me = ag[k], ot = ag[1 - k];
+        row[0] = me.x; row[1] = me.y; row[2] = me.z; row[3] = me.w;
+        row[4] = fsub(goal[k].x, me.x); row[5] = fsub(goal[k].y, me.y);
+        row[6] = fsub(ot.x, me.x); row[7] = fsub(ot.y, me.y);
+        row[8] = ot.z; row[9] = ot.w;
+        row[10] = (float)dsub_rn(a.sd[0], (double)me.x);
+        row[11] = (float)dsub_rn(a.sd[1], (double)me.y);
+      }
+      if (nvalid > 0) warp_flush(a.obs + k * a.obs_stride + e0 * O, nvalid, O, sbuf);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // flocking (scenarios/flocking.py): NA agents (dyn 0..NA-1), beacon marker
 // (entity NA, stat row 0), NO rocks (entity NA+1+r, stat row 1+r, immovable).
 // Pairs, lexicographic: for i: agents j>i, then rocks.  Optional Lidar
@@ -1338,6 +1396,14 @@ int launch_small(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_
 #define SS_CASE(n) case n: launch_step(k_wheel<n>, dim3(grid), dim3(kSmallThreads), shmem, st, a); break;
       switch (NA) { SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) }
 #undef SS_CASE
+      break;
+    }
+    case SS_SCN_GIVE_WAY: {
+      if ((a.mode & SS_DO_PHYSICS) || NA != 2) {
+        set_error("give_way: 2 agents; physics runs through ss_world_step (generic kernel)");
+        return SS_ERR_CONTRACT;
+      }
+      launch_step(k_give_way, dim3(grid), dim3(kSmallThreads), shmem, st, a);
       break;
     }
     case SS_SCN_DROPOUT: {

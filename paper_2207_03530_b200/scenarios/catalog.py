@@ -185,9 +185,12 @@ class Balance(Scenario):
 
 
 # ---------------------------------------------------------------------------
-@register("give_way")
 class GiveWay(Scenario):
-    """Two wide agents swap ends of a corridor with one recess."""
+    """Two wide agents swap ends of a corridor with one recess.
+
+    The registered "give_way" is scenarios/give_way.py (world_step +
+    k_give_way); this torch implementation supplies its world, reset and
+    heuristic and stays the generic-path restatement of the reference hooks."""
 
     max_steps = 300
 
