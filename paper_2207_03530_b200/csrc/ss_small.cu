@@ -689,6 +689,81 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_give_way(const
 }
 
 // ---------------------------------------------------------------------------
+// passage (catalog scenarios/passage.py): NA agents (dyn 0..NA-1), their
+// slots (stat rows 0..NA-1), three wall segments.  Physics is world_step's;
+// this kernel: count, reward -gap_k - f32(pen) * #touching teammates
+// (float32), done = every agent within f32(0.05) of its slot, observation
+// [x, y, vx, vy, slot - self, (f32(gap_x - float64(x)), 0 - y) per wall gap,
+// (other - self)].  sc[0] = f32 touch distance, sc[1] = f32(pen),
+// sc[2] = f32(0.05); sd[0], sd[1] = gap centres (python doubles).
+// ---------------------------------------------------------------------------
+template <int NA>
+__global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_passage(const SmallArgs a) {
+  extern __shared__ __align__(16) float smem[];
+  grid_dep_sync();
+  if (a.guard && *a.guard) return;
+  constexpr int O = 10 + 2 * (NA - 1);
+  const int64_t B = a.s.B;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = e < B;
+  float4 ag[NA];
+  float2 slot[NA];
+  int64_t steps = 0;
+#pragma unroll
+  for (int i = 0; i < NA; ++i) { ag[i] = make_float4(0.f, 0.f, 0.f, 0.f); slot[i] = make_float2(0.f, 0.f); }
+  if (valid) {
+#pragma unroll
+    for (int i = 0; i < NA; ++i) { ag[i] = a.s.dyn[i * B + e]; slot[i] = a.s.stat[i * B + e]; }
+    if (a.mode & (SS_DO_COUNT | SS_DO_DONE)) steps = a.s.step_count[e];
+  }
+  if (valid && (a.mode & SS_DO_COUNT)) { steps += 1; a.s.step_count[e] = steps; }
+  float gap[NA];
+#pragma unroll
+  for (int i = 0; i < NA; ++i) gap[i] = norm2(fsub(ag[i].x, slot[i].x), fsub(ag[i].y, slot[i].y));
+  if (valid && (a.mode & SS_DO_REWARD)) {
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      float cnt = 0.0f;   // common.contact_count: float32 sum in agent order
+#pragma unroll
+      for (int o = 0; o < NA; ++o) {
+        if (o == i) continue;
+        cnt = fadd(cnt, norm2(fsub(ag[i].x, ag[o].x), fsub(ag[i].y, ag[o].y)) <= a.sc[0] ? 1.0f : 0.0f);
+      }
+      __stcs(a.rew + i * B + e, fsub(-gap[i], fmul(a.sc[1], cnt)));
+    }
+  }
+  if (valid && (a.mode & SS_DO_DONE)) {
+    bool all = true;
+#pragma unroll
+    for (int i = 0; i < NA; ++i) all &= gap[i] < a.sc[2];
+    a.done[e] = (uint8_t)(all | (steps >= a.ph.max_steps));
+  }
+  if (a.mode & SS_DO_OBS) {
+    float* sbuf = smem + (threadIdx.x >> 5) * (32 * O);
+    float* row = sbuf + (threadIdx.x & 31) * O;
+    const int64_t e0 = e - (threadIdx.x & 31);
+    const int nvalid = (int)min((int64_t)32, B - e0);
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      if (valid) {
+        const float4 me = ag[i];
+        row[0] = me.x; row[1] = me.y; row[2] = me.z; row[3] = me.w;
+        row[4] = fsub(slot[i].x, me.x); row[5] = fsub(slot[i].y, me.y);
+        row[6] = (float)dsub_rn(a.sd[0], (double)me.x); row[7] = fsub(0.0f, me.y);
+        row[8] = (float)dsub_rn(a.sd[1], (double)me.x); row[9] = fsub(0.0f, me.y);
+        int c = 10;
+#pragma unroll
+        for (int o = 0; o < NA; ++o) {
+          if (o == i) continue;
+          row[c++] = fsub(ag[o].x, me.x); row[c++] = fsub(ag[o].y, me.y);
+        }
+      }
+      if (nvalid > 0) warp_flush(a.obs + i * a.obs_stride + e0 * O, nvalid, O, sbuf);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // flocking (scenarios/flocking.py): NA agents (dyn 0..NA-1), beacon marker
 // (entity NA, stat row 0), NO rocks (entity NA+1+r, stat row 1+r, immovable).
 // Pairs, lexicographic: for i: agents j>i, then rocks.  Optional Lidar
@@ -1404,6 +1479,16 @@ int launch_small(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_
         return SS_ERR_CONTRACT;
       }
       launch_step(k_give_way, dim3(grid), dim3(kSmallThreads), shmem, st, a);
+      break;
+    }
+    case SS_SCN_PASSAGE: {
+      if (a.mode & SS_DO_PHYSICS) {
+        set_error("passage: physics runs through ss_world_step (generic kernel)");
+        return SS_ERR_CONTRACT;
+      }
+#define SS_CASE(n) case n: launch_step(k_passage<n>, dim3(grid), dim3(kSmallThreads), shmem, st, a); break;
+      switch (NA) { SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) }
+#undef SS_CASE
       break;
     }
     case SS_SCN_DROPOUT: {

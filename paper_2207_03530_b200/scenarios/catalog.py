@@ -378,9 +378,12 @@ OFFSETS = [(0.0, 0.0), (0.2, 0.0), (-0.2, 0.0), (0.0, 0.2), (0.0, -0.2)]
 GAPS, GAP_WIDTH = (-0.6, 0.6), 0.25
 
 
-@register("passage")
 class Passage(Scenario):
-    """A cross formation squeezes through two wall gaps and reforms."""
+    """A cross formation squeezes through two wall gaps and reforms.
+
+    The registered "passage" is scenarios/passage.py (world_step +
+    k_passage); this torch implementation supplies its world, reset and
+    heuristic and stays the generic-path restatement of the reference hooks."""
 
     max_steps = 250
 
