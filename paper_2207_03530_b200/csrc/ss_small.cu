@@ -764,6 +764,65 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_passage(const 
 }
 
 // ---------------------------------------------------------------------------
+// balance (catalog scenarios/balance.py): NA agents (dyn 0..NA-1), tray
+// (entity NA, dyn row NA, rotatable), ball (dyn row NA+1), goal (stat row 0),
+// floor.  Physics (gravity, sphere-line contacts, the tray's torque) is
+// world_step's; this kernel: count, reward f32(-float64(gap) - 5 *
+// float64(ball.y < f32(floor + r + 0.02))) with gap = |ball - goal|, done =
+// gap < f32(0.08), observation [x, y, vx, vy, tray - self, cos, sin (numpy
+// float32), tray w, tray vel, ball - self, ball vel, goal - ball].
+// sc[0] = f32 drop height, sc[1] = f32(0.08).
+// ---------------------------------------------------------------------------
+template <int NA>
+__global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_balance(const SmallArgs a) {
+  extern __shared__ __align__(16) float smem[];
+  grid_dep_sync();
+  if (a.guard && *a.guard) return;
+  constexpr int O = 17;
+  const int64_t B = a.s.B;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = e < B;
+  float4 tray = make_float4(0.f, 0.f, 0.f, 0.f), ball = tray;
+  float2 trw = make_float2(0.f, 0.f), goal = trw;
+  int64_t steps = 0;
+  if (valid) {
+    tray = a.s.dyn[NA * B + e];
+    ball = a.s.dyn[(NA + 1) * B + e];
+    trw = a.s.rot[NA * B + e];
+    goal = a.s.stat[e];
+    if (a.mode & (SS_DO_COUNT | SS_DO_DONE)) steps = a.s.step_count[e];
+  }
+  if (valid && (a.mode & SS_DO_COUNT)) { steps += 1; a.s.step_count[e] = steps; }
+  const float gap = norm2(fsub(ball.x, goal.x), fsub(ball.y, goal.y));
+  if (valid && (a.mode & SS_DO_REWARD)) {
+    const float r = (float)dsub_rn(-(double)gap, ball.y < a.sc[0] ? 5.0 : 0.0);
+#pragma unroll
+    for (int i = 0; i < NA; ++i) __stcs(a.rew + i * B + e, r);
+  }
+  if (valid && (a.mode & SS_DO_DONE)) a.done[e] = (uint8_t)((gap < a.sc[1]) | (steps >= a.ph.max_steps));
+  if (a.mode & SS_DO_OBS) {
+    float* sbuf = smem + (threadIdx.x >> 5) * (32 * O);
+    float* row = sbuf + (threadIdx.x & 31) * O;
+    const int64_t e0 = e - (threadIdx.x & 31);
+    const int nvalid = (int)min((int64_t)32, B - e0);
+    const float c = valid ? np_cosf(trw.x) : 0.f, sn = valid ? np_sinf(trw.x) : 0.f;
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      if (valid) {
+        const float4 q = a.s.dyn[i * B + e];
+        row[0] = q.x; row[1] = q.y; row[2] = q.z; row[3] = q.w;
+        row[4] = fsub(tray.x, q.x); row[5] = fsub(tray.y, q.y);
+        row[6] = c; row[7] = sn; row[8] = trw.y; row[9] = tray.z; row[10] = tray.w;
+        row[11] = fsub(ball.x, q.x); row[12] = fsub(ball.y, q.y);
+        row[13] = ball.z; row[14] = ball.w;
+        row[15] = fsub(goal.x, ball.x); row[16] = fsub(goal.y, ball.y);
+      }
+      if (nvalid > 0) warp_flush(a.obs + i * a.obs_stride + e0 * O, nvalid, O, sbuf);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // flocking (scenarios/flocking.py): NA agents (dyn 0..NA-1), beacon marker
 // (entity NA, stat row 0), NO rocks (entity NA+1+r, stat row 1+r, immovable).
 // Pairs, lexicographic: for i: agents j>i, then rocks.  Optional Lidar
@@ -1487,6 +1546,16 @@ int launch_small(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_
         return SS_ERR_CONTRACT;
       }
 #define SS_CASE(n) case n: launch_step(k_passage<n>, dim3(grid), dim3(kSmallThreads), shmem, st, a); break;
+      switch (NA) { SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) }
+#undef SS_CASE
+      break;
+    }
+    case SS_SCN_BALANCE: {
+      if (a.mode & SS_DO_PHYSICS) {
+        set_error("balance: physics runs through ss_world_step (generic kernel)");
+        return SS_ERR_CONTRACT;
+      }
+#define SS_CASE(n) case n: launch_step(k_balance<n>, dim3(grid), dim3(kSmallThreads), shmem, st, a); break;
       switch (NA) { SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) }
 #undef SS_CASE
       break;

@@ -103,9 +103,12 @@ class Wheel(Scenario):
 
 
 # ---------------------------------------------------------------------------
-@register("balance")
 class Balance(Scenario):
-    """Agents carry a ball on a tray against gravity to a goal."""
+    """Agents carry a ball on a tray against gravity to a goal.
+
+    The registered "balance" is scenarios/balance.py (world_step +
+    k_balance); this torch implementation supplies its world, reset and
+    heuristic and stays the generic-path restatement of the reference hooks."""
 
     max_steps = 250
 
