@@ -14,7 +14,7 @@
 #include <cstdlib>
 
 #include "ss_bulk.cuh"
-#include "ss_internal.cuh"
+#include "ss_geometry.cuh"   // (includes ss_internal.cuh)
 
 namespace ss {
 
@@ -823,6 +823,103 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_balance(const 
 }
 
 // ---------------------------------------------------------------------------
+// waterfall (catalog scenarios/waterfall.py): NA agents (dyn 0..NA-1), basin
+// (stat row 0), NB box baffles (entities NA+1.., stat rows 1..NB).  Physics
+// (gravity, sphere-box contacts) is world_step's; this kernel: count, reward
+// f32(-float64(gap) - pen * (float64(#touching teammates) + float64 sum of
+// block bumps)), a bump = |self - closest point on the block| <= f32(r);
+// done = every agent within f32(0.2) of the basin; observation [x, y, vx, vy,
+// basin - self, (block_k - self)].  sc[0] = f32 touch distance, sc[1] =
+// f32(agent radius), sc[2] = f32(0.2); sd[0] = pen (python double); si[2] = NB.
+// ---------------------------------------------------------------------------
+constexpr int kWaterfallMaxBlocks = 8;
+
+template <int NA>
+__global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_waterfall(const SmallArgs a) {
+  extern __shared__ __align__(16) float smem[];
+  grid_dep_sync();
+  if (a.guard && *a.guard) return;
+  const int NB = a.si[2];
+  const int O = a.obs_dim;   // 6 + 2 NB
+  const int64_t B = a.s.B;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = e < B;
+  float4 ag[NA];
+  float2 basin = make_float2(0.f, 0.f);
+  float2 blk[kWaterfallMaxBlocks];
+  int64_t steps = 0;
+#pragma unroll
+  for (int i = 0; i < NA; ++i) ag[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int k = 0; k < kWaterfallMaxBlocks; ++k) blk[k] = make_float2(0.f, 0.f);
+  if (valid) {
+#pragma unroll
+    for (int i = 0; i < NA; ++i) ag[i] = a.s.dyn[i * B + e];
+    basin = a.s.stat[e];
+#pragma unroll
+    for (int k = 0; k < kWaterfallMaxBlocks; ++k)
+      if (k < NB) blk[k] = a.s.stat[(1 + k) * B + e];
+    if (a.mode & (SS_DO_COUNT | SS_DO_DONE)) steps = a.s.step_count[e];
+  }
+  if (valid && (a.mode & SS_DO_COUNT)) { steps += 1; a.s.step_count[e] = steps; }
+  float gap[NA];
+#pragma unroll
+  for (int i = 0; i < NA; ++i) gap[i] = norm2(fsub(ag[i].x, basin.x), fsub(ag[i].y, basin.y));
+  if (valid && (a.mode & SS_DO_REWARD)) {
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      float cnt = 0.0f;   // common.contact_count: float32 sum in agent order
+#pragma unroll
+      for (int o = 0; o < NA; ++o) {
+        if (o == i) continue;
+        cnt = fadd(cnt, norm2(fsub(ag[i].x, ag[o].x), fsub(ag[i].y, ag[o].y)) <= a.sc[0] ? 1.0f : 0.0f);
+      }
+      double bumps = 0.0;  // _block_bumps: float64 count in block order
+      const SsEntityDesc& da = a.ents[i];
+      ShapeK sa;
+      sa.kind = da.shape; sa.d0 = da.dim0; sa.d1 = da.dim1;
+      const V2 pa = v2(ag[i].x, ag[i].y);
+      const float ra = a.s.rot[i * B + e].x;
+      for (int k = 0; k < NB; ++k) {
+        const SsEntityDesc& db = a.ents[NA + 1 + k];
+        ShapeK sb;
+        sb.kind = db.shape; sb.d0 = db.dim0; sb.d1 = db.dim1;
+        V2 oa, ob;
+        closest_points(pa, ra, sa, v2(blk[k].x, blk[k].y), a.s.rot[(NA + 1 + k) * B + e].x, sb, oa, ob);
+        bumps = dadd_rn(bumps, norm2(fsub(pa.x, ob.x), fsub(pa.y, ob.y)) <= a.sc[1] ? 1.0 : 0.0);
+      }
+      const double b = dadd_rn((double)cnt, bumps);
+      __stcs(a.rew + i * B + e, (float)dsub_rn(-(double)gap[i], dmul_rn(a.sd[0], b)));
+    }
+  }
+  if (valid && (a.mode & SS_DO_DONE)) {
+    bool all = true;
+#pragma unroll
+    for (int i = 0; i < NA; ++i) all &= gap[i] < a.sc[2];
+    a.done[e] = (uint8_t)(all | (steps >= a.ph.max_steps));
+  }
+  if (a.mode & SS_DO_OBS) {
+    const int P = O | 1;
+    float* sbuf = smem + (threadIdx.x >> 5) * (32 * P);
+    float* row = sbuf + (threadIdx.x & 31) * P;
+    const int64_t e0 = e - (threadIdx.x & 31);
+    const int nvalid = (int)min((int64_t)32, B - e0);
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      if (valid) {
+        const float4 me = ag[i];
+        row[0] = me.x; row[1] = me.y; row[2] = me.z; row[3] = me.w;
+        row[4] = fsub(basin.x, me.x); row[5] = fsub(basin.y, me.y);
+#pragma unroll
+        for (int k = 0; k < kWaterfallMaxBlocks; ++k)
+          if (k < NB) { row[6 + 2 * k] = fsub(blk[k].x, me.x); row[7 + 2 * k] = fsub(blk[k].y, me.y); }
+      }
+      if (nvalid > 0) warp_flush_padded(a.obs + i * a.obs_stride + e0 * O, nvalid, O, P, sbuf);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // flocking (scenarios/flocking.py): NA agents (dyn 0..NA-1), beacon marker
 // (entity NA, stat row 0), NO rocks (entity NA+1+r, stat row 1+r, immovable).
 // Pairs, lexicographic: for i: agents j>i, then rocks.  Optional Lidar
@@ -1556,6 +1653,17 @@ int launch_small(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_
         return SS_ERR_CONTRACT;
       }
 #define SS_CASE(n) case n: launch_step(k_balance<n>, dim3(grid), dim3(kSmallThreads), shmem, st, a); break;
+      switch (NA) { SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) }
+#undef SS_CASE
+      break;
+    }
+    case SS_SCN_WATERFALL: {
+      if ((a.mode & SS_DO_PHYSICS) || w.d.si[2] > kWaterfallMaxBlocks) {
+        set_error("waterfall: at most 8 blocks; physics runs through ss_world_step (generic kernel)");
+        return SS_ERR_CONTRACT;
+      }
+      const size_t wshm = (size_t)kSmallThreads * (w.d.obs_dim | 1) * sizeof(float);
+#define SS_CASE(n) case n: launch_step(k_waterfall<n>, dim3(grid), dim3(kSmallThreads), wshm, st, a); break;
       switch (NA) { SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) }
 #undef SS_CASE
       break;

@@ -574,9 +574,12 @@ BLOCKS = [(-0.7, 0.35), (0.0, 0.35), (0.7, 0.35), (-0.35, -0.25), (0.35, -0.25)]
 BLOCK_LEN, BLOCK_WID, BASIN = 0.45, 0.1, (0.0, -0.9)
 
 
-@register("waterfall")
 class Waterfall(Scenario):
-    """Agents drift down under gravity through staggered baffles to a basin."""
+    """Agents drift down under gravity through staggered baffles to a basin.
+
+    The registered "waterfall" is scenarios/waterfall.py (world_step +
+    k_waterfall); this torch implementation supplies its world, reset and
+    heuristic and stays the generic-path restatement of the reference hooks."""
 
     max_steps = 200
 
