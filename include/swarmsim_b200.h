@@ -58,7 +58,8 @@ typedef enum SsScenario {
   SS_SCN_GIVE_WAY = 8,         /* scenarios/give_way.py (catalog): reward/obs kernel; physics by world_step */
   SS_SCN_PASSAGE = 9,          /* scenarios/passage.py (catalog): reward/obs kernel; physics by world_step */
   SS_SCN_BALANCE = 10,         /* scenarios/balance.py (catalog): reward/obs kernel; physics by world_step */
-  SS_SCN_WATERFALL = 11        /* scenarios/waterfall.py (catalog): reward/obs kernel; physics by world_step */
+  SS_SCN_WATERFALL = 11,       /* scenarios/waterfall.py (catalog): reward/obs kernel; physics by world_step */
+  SS_SCN_FOOTBALL = 12         /* scenarios/football.py (catalog): reward/obs kernel; physics by world_step */
 } SsScenario;
 
 /* Step phases (bit flags of SsStepIO.mode). A full Env.step is SS_MODE_STEP. */

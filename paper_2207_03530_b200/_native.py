@@ -20,7 +20,7 @@ RNG_WORDS = 12
 
 SS_SPHERE, SS_BOX, SS_LINE = 0, 1, 2
 (SCN_PHYSICS_ONLY, SCN_SIMPLE_SPREAD, SCN_TRANSPORT, SCN_FLOCKING, SCN_DISPERSION, SCN_DISCOVERY, SCN_DROPOUT,
- SCN_WHEEL, SCN_GIVE_WAY, SCN_PASSAGE, SCN_BALANCE, SCN_WATERFALL) = range(12)
+ SCN_WHEEL, SCN_GIVE_WAY, SCN_PASSAGE, SCN_BALANCE, SCN_WATERFALL, SCN_FOOTBALL) = range(13)
 
 DO_PHYSICS, DO_POST, DO_COUNT, DO_REWARD, DO_DONE, DO_OBS = 1, 2, 4, 8, 16, 32
 MODE_STEP = 63

@@ -78,7 +78,7 @@ static int validate_desc(const SsWorldDesc* d) {
   if (d->global_batch < d->batch || d->env_offset < 0 || d->env_offset + d->batch > d->global_batch) {
     set_error("shard [env_offset, env_offset+batch) outside global_batch"); return SS_ERR_CONTRACT;
   }
-  if (d->scenario < SS_SCN_PHYSICS_ONLY || d->scenario > SS_SCN_WATERFALL) {
+  if (d->scenario < SS_SCN_PHYSICS_ONLY || d->scenario > SS_SCN_FOOTBALL) {
     set_error("unknown scenario id " + std::to_string(d->scenario)); return SS_ERR_SCENARIO;
   }
   if (d->n_reset_ops < 0 || d->n_reset_ops > SS_MAX_RESET_OPS) { set_error("bad reset program"); return SS_ERR_CONTRACT; }
@@ -170,6 +170,7 @@ int ss_env_step(void* world, const SsBuffers* buf, const SsStepIO* io, void* str
     case SS_SCN_PASSAGE:
     case SS_SCN_BALANCE:
     case SS_SCN_WATERFALL:
+    case SS_SCN_FOOTBALL:
       return launch_small(*w, buf, io, st);
     case SS_SCN_DISPERSION:
     case SS_SCN_DISCOVERY:

@@ -920,6 +920,78 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_waterfall(cons
 }
 
 // ---------------------------------------------------------------------------
+// football (catalog scenarios/football.py): NA = 2 NT agents — blues
+// 0..NT-1 (controlled), reds NT..NA-1 (scripted: their forces come from the
+// host script, decoded before world_step) — ball (dyn row NA), 12 walls.
+// Physics is world_step's; this kernel: count, reward for blues
+// f32(10 * right - 10 * left - float64(f32(0.1) * |ball - (hx, 0)|)), 0 for
+// reds, done = right | left (ball beyond -/+ f32(hx + 0.04)), observation
+// [x, y, vx, vy, ball - self, ball vel, (mate - self), (foe - self),
+// f32(attack_x - float64(x)), 0 - y].  sc[0] = f32(hx + 0.04), sc[1] =
+// f32(0.1), sc[2] = f32(hx); sd[0] = hx (python double).
+// ---------------------------------------------------------------------------
+template <int NA>
+__global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_football(const SmallArgs a) {
+  extern __shared__ __align__(16) float smem[];
+  grid_dep_sync();
+  if (a.guard && *a.guard) return;
+  constexpr int NT = NA / 2;
+  constexpr int O = 4 + 2 + 2 + 2 * (NA - 1) + 2;
+  const int64_t B = a.s.B;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = e < B;
+  float4 ag[NA], ball = make_float4(0.f, 0.f, 0.f, 0.f);
+  int64_t steps = 0;
+#pragma unroll
+  for (int i = 0; i < NA; ++i) ag[i] = ball;
+  if (valid) {
+#pragma unroll
+    for (int i = 0; i < NA; ++i) ag[i] = a.s.dyn[i * B + e];
+    ball = a.s.dyn[NA * B + e];
+    if (a.mode & (SS_DO_COUNT | SS_DO_DONE)) steps = a.s.step_count[e];
+  }
+  if (valid && (a.mode & SS_DO_COUNT)) { steps += 1; a.s.step_count[e] = steps; }
+  const bool right = ball.x > a.sc[0], left = ball.x < -a.sc[0];
+  if (valid && (a.mode & SS_DO_REWARD)) {
+    const float gap = norm2(fsub(ball.x, a.sc[2]), fsub(ball.y, 0.0f));
+    const double r = dsub_rn(dsub_rn(right ? 10.0 : 0.0, left ? 10.0 : 0.0), (double)fmul(a.sc[1], gap));
+#pragma unroll
+    for (int i = 0; i < NA; ++i) __stcs(a.rew + i * B + e, i < NT ? (float)r : 0.0f);
+  }
+  if (valid && (a.mode & SS_DO_DONE)) a.done[e] = (uint8_t)((right | left) | (steps >= a.ph.max_steps));
+  if (a.mode & SS_DO_OBS) {
+    float* sbuf = smem + (threadIdx.x >> 5) * (32 * O);
+    float* row = sbuf + (threadIdx.x & 31) * O;
+    const int64_t e0 = e - (threadIdx.x & 31);
+    const int nvalid = (int)min((int64_t)32, B - e0);
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      if (valid) {
+        const float4 me = ag[i];
+        const bool blue = i < NT;
+        row[0] = me.x; row[1] = me.y; row[2] = me.z; row[3] = me.w;
+        row[4] = fsub(ball.x, me.x); row[5] = fsub(ball.y, me.y);
+        row[6] = ball.z; row[7] = ball.w;
+        int c = 8;
+#pragma unroll
+        for (int o = 0; o < NA; ++o) {          // mates, world order
+          if (o == i || (o < NT) != blue) continue;
+          row[c++] = fsub(ag[o].x, me.x); row[c++] = fsub(ag[o].y, me.y);
+        }
+#pragma unroll
+        for (int o = 0; o < NA; ++o) {          // foes, world order
+          if ((o < NT) == blue) continue;
+          row[c++] = fsub(ag[o].x, me.x); row[c++] = fsub(ag[o].y, me.y);
+        }
+        row[c] = (float)dsub_rn(blue ? a.sd[0] : -a.sd[0], (double)me.x);
+        row[c + 1] = fsub(0.0f, me.y);
+      }
+      if (nvalid > 0) warp_flush(a.obs + i * a.obs_stride + e0 * O, nvalid, O, sbuf);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // flocking (scenarios/flocking.py): NA agents (dyn 0..NA-1), beacon marker
 // (entity NA, stat row 0), NO rocks (entity NA+1+r, stat row 1+r, immovable).
 // Pairs, lexicographic: for i: agents j>i, then rocks.  Optional Lidar
@@ -1665,6 +1737,16 @@ int launch_small(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_
       const size_t wshm = (size_t)kSmallThreads * (w.d.obs_dim | 1) * sizeof(float);
 #define SS_CASE(n) case n: launch_step(k_waterfall<n>, dim3(grid), dim3(kSmallThreads), wshm, st, a); break;
       switch (NA) { SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) }
+#undef SS_CASE
+      break;
+    }
+    case SS_SCN_FOOTBALL: {
+      if ((a.mode & SS_DO_PHYSICS) || (NA & 1)) {
+        set_error("football: two equal teams; physics runs through ss_world_step (generic kernel)");
+        return SS_ERR_CONTRACT;
+      }
+#define SS_CASE(n) case n: launch_step(k_football<n>, dim3(grid), dim3(kSmallThreads), shmem, st, a); break;
+      switch (NA) { SS_CASE(2) SS_CASE(4) SS_CASE(6) SS_CASE(8) }
 #undef SS_CASE
       break;
     }

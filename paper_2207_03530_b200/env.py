@@ -420,16 +420,16 @@ class StepGraph:
         if env.action_mode != "continuous" or any(s.comm_dim for s in env.action_specs) or env._any_obs_noise \
                 or any(a.action_noise_std > 0.0 for a in env.agents):
             raise ContractViolation("StepGraph covers continuous, noiseless, silent agents")
-        if env.fused and env._needs_host_decode([0] * A):
-            raise ContractViolation("StepGraph on a built-in scenario covers unscripted agents")
         self.env = env
         self.actions = acts
         self.steps_per_replay = S
-        self._generic = not env.fused
+        # scripted agents (or a non-fused scenario): capture the whole public
+        # step — scripts, decode, launches — instead of the bare fused launch
+        self._generic = not env.fused or env._needs_host_decode([0] * A)
         sc, world = env.scenario, env.world
         self._rng_mode = bool(getattr(sc, "advances_rng_per_step", False))
         world.ensure_device_rng()
-        if self._generic:
+        if not env.fused:
             # generic worlds: physics through ss_world_step plus the scenario's
             # torch hooks; they must not sync with the host or draw from the
             # Env stream inside step (checked: a draw raises during capture)
@@ -487,8 +487,8 @@ class StepGraph:
         env.validate = False
         rng.capture_guard = True
         try:
-            return env._step_generic([None if a.action_script is not None else act[n]
-                                      for n, a in enumerate(env.agents)])
+            raw = [None if a.action_script is not None else act[n] for n, a in enumerate(env.agents)]
+            return env._step_fused(raw) if env.fused else env._step_generic(raw)
         finally:
             env.validate = saved
             rng.capture_guard = False

@@ -21,7 +21,6 @@ from ..core import Agent, AgentAction, Entity, PhysParams, World
 from ..env import Scenario
 from ..geometry import closest_points
 from ..shapes import Box, Line, Sphere, min_contact_distance
-from . import register
 from .common import clip_unit, columns, contact_count, marker, place, pos_vel, rel_pos, scatter, unit
 
 F64 = torch.float64
@@ -281,9 +280,13 @@ def chase_script(agent: Agent, world: World) -> AgentAction:
     return AgentAction(force=Vec2(fx * agent.u_multiplier, fy * agent.u_multiplier))
 
 
-@register("football")
 class Football(Scenario):
-    """Two-a-side: the controlled blue team attacks against scripted reds."""
+    """Two-a-side: the controlled blue team attacks against scripted reds.
+
+    The registered "football" is scenarios/football.py (world_step +
+    k_football); this torch implementation supplies its world, reset, the
+    reds' script and the heuristic, and stays the generic-path restatement of
+    the reference hooks."""
 
     max_steps = 400
 

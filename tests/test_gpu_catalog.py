@@ -117,7 +117,7 @@ def test_generic_step_graph_equals_eager(cuda, name):
 
 @pytest.mark.parametrize("name", ["simple_spread", "transport", "flocking", "dispersion", "discovery",
                                   "reverse_transport", "dropout", "wheel", "give_way", "passage",
-                                  "balance", "waterfall"])
+                                  "balance", "waterfall", "football"])
 def test_fused_hooks_equal_step_outputs(cuda, name):
     """The reference's Scenario hooks on a fused world (single-phase kernel
     launches: reward, done, observation) reproduce what Env.step returned —
