@@ -1062,6 +1062,7 @@ struct RayFan {
   float quarter;    // (pi / 2) / step
   uint32_t all;     // bits 0..n-1
   int n;
+  int full;         // span == 2 pi: period == n, windows wrap by rotation
 };
 
 // atan2 with |error| < 2e-6 rad over all quadrants (checked on the host
@@ -1112,6 +1113,16 @@ SS_DEV uint32_t ray_window(float fx, float fy, const RayFan& fan, const RayScree
   if (!(w < fan.quarter)) return fan.all;
   float v = __fmul_rn(__fsub_rn(fast_atan2(-fy, -fx), fan.start), fan.inv_step);
   v = __fsub_rn(v, __fmul_rn(fan.period, floorf(__fdividef(v, fan.period))));
+  if (fan.full) {
+    // rays lo..hi modulo n: one contiguous run rotated into place
+    const int lo = (int)ceilf(v - w), hi = (int)floorf(v + w);   // -n/4 <= lo, hi < 5n/4
+    const int cnt = hi - lo + 1;
+    if (cnt <= 0) return 0u;
+    if (cnt >= fan.n) return fan.all;
+    const int base = lo < 0 ? lo + fan.n : (lo >= fan.n ? lo - fan.n : lo);
+    const uint64_t m = (uint64_t)((1u << cnt) - 1u) << base;
+    return (uint32_t)(m | (m >> fan.n)) & fan.all;
+  }
   return ray_bits(v - w, v + w, fan.n) | ray_bits(v - w + fan.period, v + w + fan.period, fan.n) |
          ray_bits(v - w - fan.period, v + w - fan.period, fan.n);
 }
@@ -1788,6 +1799,7 @@ int launch_small(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_
         lk.fan.quarter = (float)(0.25 * two_pi / step);
         lk.fan.n = a.n_rays;
         lk.fan.all = a.n_rays >= 32 ? 0xffffffffu : ((1u << a.n_rays) - 1u);
+        lk.fan.full = span == two_pi && lk.fan.period == (float)a.n_rays;
       }
       static const bool legacy = std::getenv("SS_FLOCK_THREAD_PER_ENV") != nullptr;
       if (!legacy) {
