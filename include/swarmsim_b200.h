@@ -29,11 +29,13 @@
 extern "C" {
 #endif
 
-#define SS_ABI_VERSION 1
+#define SS_ABI_VERSION 2
 #define SS_RNG_WORDS 12          /* counter[4] key[2] buffer[4] buffer_pos spare */
 #define SS_MAX_ENTITIES 1024
 #define SS_MAX_AGENTS 256
 #define SS_MAX_RESET_OPS 1024
+#define SS_MAX_JOINTS 1024
+#define SS_MAX_SUBSTEPS 1024
 
 typedef enum SsStatus {
   SS_OK = 0,
@@ -106,6 +108,25 @@ typedef struct SsResetOp {
   double range_x, range_y;/* scatter: hi - lo (float64, as numpy computes)    */
 } SsResetOp;
 
+/* Distance joint (extension; the reference has none — SPEC.md:204 lists
+ * joints as a non-goal).  VMAS-style penalty constraint between anchor points
+ * of entities a and b: anchor = pos + R(rot) * (ox, oy) (body-frame offsets,
+ * float32).  With delta = anchor_a - anchor_b and dist = |delta|, a pair of
+ * softplus penalties keeps dist at `dist`: repulsive when dist < target,
+ * attractive when dist > target, none when dist < 1e-6 or dist == target.
+ *   z   = |target - dist| / k,   pen = softplus(z) * k   (k = contact_margin)
+ *   f_a = s * stiffness * (delta / dist) * pen,  s = +1 repulsive, -1 attractive
+ *   f_b = -f_a; torques r x f on rotatable ends when rotate_a / rotate_b.
+ * Joint forces are added after every pair contact, in joint-list order. */
+typedef struct SsJointDesc {
+  int32_t a, b;           /* entity indices (a != b)                          */
+  float ox_a, oy_a;       /* anchor offset on a, body frame (f32)             */
+  float ox_b, oy_b;       /* anchor offset on b, body frame (f32)             */
+  float dist;             /* f32 target distance between the anchors          */
+  float stiffness;        /* f32 force multiplier                             */
+  int32_t rotate_a, rotate_b;  /* apply the joint torque to a / b             */
+} SsJointDesc;
+
 typedef struct SsWorldDesc {
   int32_t abi_version;    /* SS_ABI_VERSION */
   int32_t scenario;       /* SsScenario */
@@ -137,6 +158,15 @@ typedef struct SsWorldDesc {
   double lidar_max_range;
   double lidar_start, lidar_span;
   const double* lidar_dirs;   /* HOST [lidar_rays][2]: numpy cos/sin of the rot=0 angles */
+  /* ABI 2 extensions (both default to the reference's behaviour) */
+  int32_t substeps;       /* physics sub-steps per Env.step (>= 1; 1 = reference).
+                             dt, inv_m_dt, inv_i_dt are already the SUB-step
+                             values f32(dt / substeps); keep stays f32(1 - damping)
+                             per sub-step (VMAS semantics). Actions, scripts,
+                             post_step, rewards, dones and observations run once. */
+  int32_t n_joints;       /* 0 = none (reference); worlds with joints run the
+                             generic physics kernel */
+  const SsJointDesc* joints;
 } SsWorldDesc;
 
 /* Device state, all row-major [row][B][...], env index contiguous. */
@@ -236,9 +266,12 @@ int ss_closest_points(const float* pos_i /*[n][2]*/, const float* rot_i, int32_t
  * world: forces[a] is agent a's force [B][2] (device); decode_mask bit a
  * (4 x uint64, NULL = all) applies decode_action's clip*u_multiplier to it
  * (Env.step path) instead of using it as-is (AgentAction / action_script
- * path).  count != 0 also increments step_count.  *d_status as above. */
+ * path).  count != 0 also increments step_count.  guard (device, may be
+ * NULL): if *guard != 0 the launch leaves every buffer untouched (the NaN
+ * verdict of ss_check_actions, env.py:85).  *d_status as above. */
 int ss_world_step(void* world, const SsBuffers* buf, const float* const* forces,
-                  const uint64_t* decode_mask, int32_t count, int32_t* d_status, void* stream);
+                  const uint64_t* decode_mask, int32_t count, const int32_t* guard,
+                  int32_t* d_status, void* stream);
 
 #ifdef __cplusplus
 }

@@ -15,7 +15,7 @@ from pathlib import Path
 from .errors import ContractViolation, NativeError, UnknownScenario, UnsupportedShapePair
 
 LIB_PATH = Path(os.environ.get("SS_LIB_PATH") or Path(__file__).resolve().parent / "libswarmsim_b200.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 RNG_WORDS = 12
 
 SS_SPHERE, SS_BOX, SS_LINE = 0, 1, 2
@@ -47,6 +47,12 @@ class SsResetOp(ctypes.Structure):
                 ("range_x", c_f64), ("range_y", c_f64)]
 
 
+class SsJointDesc(ctypes.Structure):
+    _fields_ = [("a", c_i32), ("b", c_i32), ("ox_a", c_f32), ("oy_a", c_f32), ("ox_b", c_f32),
+                ("oy_b", c_f32), ("dist", c_f32), ("stiffness", c_f32), ("rotate_a", c_i32),
+                ("rotate_b", c_i32)]
+
+
 class SsWorldDesc(ctypes.Structure):
     _fields_ = [
         ("abi_version", c_i32), ("scenario", c_i32), ("n_entities", c_i32), ("n_agents", c_i32),
@@ -60,6 +66,7 @@ class SsWorldDesc(ctypes.Structure):
         ("lidar_rays", c_i32), ("lidar_attach_rotation", c_i32),
         ("lidar_max_range", c_f64), ("lidar_start", c_f64), ("lidar_span", c_f64),
         ("lidar_dirs", ctypes.POINTER(c_f64)),
+        ("substeps", c_i32), ("n_joints", c_i32), ("joints", ctypes.POINTER(SsJointDesc)),
     ]
 
 
@@ -90,7 +97,7 @@ def _declare(lib) -> None:
     lib.ss_world_create.argtypes = [P(SsWorldDesc), P(c_vp)]
     lib.ss_world_destroy.argtypes = [c_vp]
     lib.ss_env_step.argtypes = [c_vp, P(SsBuffers), P(SsStepIO), c_vp]
-    lib.ss_world_step.argtypes = [c_vp, P(SsBuffers), P(c_vp), P(ctypes.c_uint64), c_i32, c_vp, c_vp]
+    lib.ss_world_step.argtypes = [c_vp, P(SsBuffers), P(c_vp), P(ctypes.c_uint64), c_i32, c_vp, c_vp, c_vp]
     lib.ss_reset.argtypes = [c_vp, P(SsBuffers), c_vp, c_vp, c_vp, c_vp]
     lib.ss_mask_count.argtypes = [c_vp, c_vp, c_vp, c_vp]
     lib.ss_check_actions.argtypes = [c_vp, P(c_vp), c_vp, c_vp]

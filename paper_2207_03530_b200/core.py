@@ -33,15 +33,34 @@ from .shapes import Shape, Sphere, min_contact_distance, native_shape
 
 @dataclass
 class PhysParams:
-    """World constants (core.py:20-44): dt, damping, gravity, contact c and k."""
+    """World constants (core.py:20-44): dt, damping, gravity, contact c and k.
+
+    substeps (extension, default 1 = the reference): physics sub-steps per
+    Env.step.  Each sub-step re-evaluates every contact / joint force on the
+    current state and integrates with the sub-step dt f32(dt / substeps),
+    keeping damping per sub-step (VMAS semantics); actions and scripts are
+    decoded once per step and held, post_step / rewards / dones /
+    observations run once after the last sub-step.  One step with substeps=k
+    equals k reference world_step calls with PhysParams(dt=dt/k) on the same
+    decoded actions (tests/test_gpu_physics.py pins it that way).
+    """
 
     dt: float = 0.1
     damping: float = 0.25
     gravity: tuple = (0.0, 0.0)
     contact_force: float = 100.0
     contact_margin: float = 1e-3
+    substeps: int = 1
+
+    @property
+    def sub_dt(self) -> float:
+        """The integrator's dt: dt / substeps (python double, cast at use)."""
+        return self.dt / self.substeps if self.substeps != 1 else self.dt
 
     def __post_init__(self):
+        if int(self.substeps) != self.substeps or not 1 <= self.substeps <= 1024:
+            raise ContractViolation(f"substeps must be an integer in [1, 1024], got {self.substeps}")
+        self.substeps = int(self.substeps)
         if not self.dt > 0:
             raise ContractViolation(f"dt must be positive, got {self.dt}")
         if not 0 <= self.damping < 1:
@@ -270,6 +289,50 @@ class Agent(Entity):
 Landmark = Entity   # VMAS vocabulary: a non-agent entity
 
 
+class Joint:
+    """Distance joint between two entities (extension: the reference has no
+    joints; VMAS-style penalty constraint, off unless added).
+
+    Anchors are body-frame offsets normalised to the entity's extent, as in
+    VMAS: anchor (1, 0) is the +x tip of a line / box half length (or the
+    sphere's radius).  The joint holds the anchors at `dist` apart with a
+    softplus penalty of multiplier `stiffness` (default 130, VMAS's
+    joint_force): attractive when stretched, repulsive when compressed.
+    rotate_a / rotate_b apply its torque to rotatable ends.  Exact arithmetic:
+    include/swarmsim_b200.h SsJointDesc; parity is pinned to the numpy
+    restatement oracle/swarm_oracle.py joint_forces (unpinned by the reference).
+    """
+
+    def __init__(self, entity_a: "Entity", entity_b: "Entity", anchor_a=(0.0, 0.0), anchor_b=(0.0, 0.0),
+                 dist: float = 0.0, stiffness: float = 130.0, rotate_a: bool = True, rotate_b: bool = True):
+        if entity_a is entity_b:
+            raise ContractViolation("a joint needs two distinct entities")
+        if not dist >= 0.0:
+            raise ContractViolation(f"joint dist must be non-negative, got {dist}")
+        if not stiffness >= 0.0:
+            raise ContractViolation(f"joint stiffness must be non-negative, got {stiffness}")
+        self.entity_a, self.entity_b = entity_a, entity_b
+        self.anchor_a = (float(anchor_a[0]), float(anchor_a[1]))
+        self.anchor_b = (float(anchor_b[0]), float(anchor_b[1]))
+        self.dist = float(dist)
+        self.stiffness = float(stiffness)
+        self.rotate_a, self.rotate_b = bool(rotate_a), bool(rotate_b)
+
+    @staticmethod
+    def offset(entity: "Entity", anchor) -> tuple:
+        """Body-frame offset of a normalised anchor (float32): extent * anchor."""
+        from .shapes import Box, Line
+
+        sh = entity.shape
+        if isinstance(sh, Box):
+            hx, hy = sh.length / 2, sh.width / 2
+        elif isinstance(sh, Line):
+            hx, hy = sh.length / 2, 0.0
+        else:
+            hx = hy = sh.radius
+        return np.float32(anchor[0] * hx), np.float32(anchor[1] * hy)
+
+
 def _collidable_pairs(world: "World") -> list[tuple[int, int]]:
     """Static pair list (dynamics.py:89-100): both collidable, one can move."""
     ents = world.entities
@@ -294,12 +357,13 @@ class World:
             raise ContractViolation(f"batch_size must be >= 1, got {batch_size}")
         self.batch_size = int(batch_size)
         self.device = torch.device(device) if device is not None else default_device()
-        self.params = params if params is not None else PhysParams()
+        self._params = params if params is not None else PhysParams()
         self.rng = rng if rng is not None else SeededRng(seed)
         self.entities: list[Entity] = []
         self._names: set[str] = set()
         self._pairs: list[tuple[int, int]] | None = None
         self.comm: dict = {}
+        self.joints: list[Joint] = []
         # sharding: this world holds global envs [env_offset, env_offset + B)
         self.env_offset = 0
         self.global_batch = self.batch_size
@@ -313,8 +377,20 @@ class World:
         self.flags = torch.zeros((1, self.batch_size), dtype=torch.int32, device=self.device)
         self.aux = torch.zeros(self.batch_size, dtype=torch.float32, device=self.device)
         self.version = 0
+        self.native_epoch = 0
         self._native_cache: dict = {}
         self._buf_cache = None
+
+    @property
+    def params(self) -> PhysParams:
+        return self._params
+
+    @params.setter
+    def params(self, p: PhysParams) -> None:
+        """Replace the physics constants (rebuilds the native descriptor)."""
+        self._params = p
+        if hasattr(self, "_native_cache"):
+            self._touch()
 
     # -- entity bookkeeping ---------------------------------------------------
     @property
@@ -337,6 +413,16 @@ class World:
         entity.state = EntityState(self, entity)
         self._relayout(new=entity)
         return entity
+
+    def add_joint(self, joint: Joint) -> Joint:
+        """Attach a joint constraint (extension; worlds with joints step their
+        physics in the generic kernel)."""
+        for e in (joint.entity_a, joint.entity_b):
+            if id(e) not in self._index:
+                raise ContractViolation(f"joint end {e.name!r} is not in this world")
+        self.joints.append(joint)
+        self._touch()
+        return joint
 
     def entity(self, name: str) -> Entity:
         for e in self.entities:
@@ -441,9 +527,12 @@ class World:
 
     # -- native descriptor ----------------------------------------------------
     def _drop_native(self) -> None:
+        """Free every cached SsWorld.  Bumps native_epoch: a StepGraph captured
+        before refuses to replay (its kernels hold the freed tables)."""
         for h in self._native_cache.values():
             h.close()
         self._native_cache.clear()
+        self.native_epoch += 1
 
     def ensure_flag_words(self, n: int) -> None:
         if self.flags.shape[0] < max(1, n):
@@ -452,7 +541,7 @@ class World:
 
     def entity_descs(self):
         p = self.params
-        dt = np.float32(p.dt)
+        dt = np.float32(p.sub_dt)
         gx, gy = p.gravity
         arr = (N.SsEntityDesc * max(1, len(self.entities)))()
         for k, e in enumerate(self.entities):
@@ -507,8 +596,9 @@ class World:
         d.env_offset = self.env_offset
         d.global_batch = self.global_batch
         d.max_steps = int(max_steps)
-        d.dt = np.float32(p.dt)
+        d.dt = np.float32(p.sub_dt)
         d.keep = np.float32(1.0 - p.damping)
+        d.substeps = p.substeps
         d.contact_ck = np.float32(p.contact_force * p.contact_margin)
         d.contact_k = np.float32(p.contact_margin)
         d.has_gravity = int(p.gravity[0] != 0.0 or p.gravity[1] != 0.0)
@@ -517,8 +607,23 @@ class World:
         d.entities = ctypes.cast(ents, ctypes.POINTER(N.SsEntityDesc))
         d.pairs = ctypes.cast(pairs, ctypes.POINTER(N.SsPairDesc))
         d.n_pairs = n_pairs
-        d._keep = (ents, pairs)   # keep ctypes arrays alive until ss_world_create copies them
+        joints = self.joint_descs()
+        d.n_joints = len(self.joints)
+        d.joints = ctypes.cast(joints, ctypes.POINTER(N.SsJointDesc))
+        d._keep = (ents, pairs, joints)   # keep ctypes arrays alive until ss_world_create copies them
         return d
+
+    def joint_descs(self):
+        arr = (N.SsJointDesc * max(1, len(self.joints)))()
+        for n, jt in enumerate(self.joints):
+            q = arr[n]
+            q.a, q.b = self._index[id(jt.entity_a)], self._index[id(jt.entity_b)]
+            q.ox_a, q.oy_a = Joint.offset(jt.entity_a, jt.anchor_a)
+            q.ox_b, q.oy_b = Joint.offset(jt.entity_b, jt.anchor_b)
+            q.dist = np.float32(jt.dist)
+            q.stiffness = np.float32(jt.stiffness)
+            q.rotate_a, q.rotate_b = int(jt.rotate_a), int(jt.rotate_b)
+        return arr
 
     def buffers(self) -> "N.SsBuffers":
         b = N.SsBuffers()

@@ -60,6 +60,7 @@ static void free_world(World* w) {
   cudaFree(w->d_reset_ops);
   cudaFree(w->d_lidar_dirs);
   cudaFree(w->d_scan);
+  cudaFree(w->d_joints);
   delete w;
 }
 
@@ -95,6 +96,18 @@ static int validate_desc(const SsWorldDesc* d) {
     const SsPairDesc& q = d->pairs[p];
     if (q.i < 0 || q.j <= q.i || q.j >= d->n_entities) { set_error("bad pair list"); return SS_ERR_CONTRACT; }
   }
+  if (d->substeps < 1 || d->substeps > SS_MAX_SUBSTEPS) {
+    set_error("substeps must be in [1, " + std::to_string(SS_MAX_SUBSTEPS) + "]"); return SS_ERR_CONTRACT;
+  }
+  if (d->n_joints < 0 || d->n_joints > SS_MAX_JOINTS || (d->n_joints > 0 && !d->joints)) {
+    set_error("bad joint table"); return SS_ERR_CONTRACT;
+  }
+  for (int j = 0; j < d->n_joints; ++j) {
+    const SsJointDesc& q = d->joints[j];
+    if (q.a < 0 || q.b < 0 || q.a >= d->n_entities || q.b >= d->n_entities || q.a == q.b) {
+      set_error("joint " + std::to_string(j) + " has bad entity indices"); return SS_ERR_CONTRACT;
+    }
+  }
   for (int j = 0; j < d->n_reset_ops; ++j) {
     const SsResetOp& o = d->reset_ops[j];
     if (o.entity < 0 || o.entity >= d->n_entities || (o.kind != 0 && o.kind != 1)) {
@@ -125,10 +138,11 @@ int ss_world_create(const SsWorldDesc* desc, void** out_world) {
   w->ents.assign(desc->entities, desc->entities + desc->n_entities);
   w->pairs.assign(desc->pairs, desc->pairs + desc->n_pairs);
   w->reset_ops.assign(desc->reset_ops, desc->reset_ops + desc->n_reset_ops);
+  if (desc->n_joints > 0) w->joints.assign(desc->joints, desc->joints + desc->n_joints);
   w->n_scatter = 0;
   for (const auto& o : w->reset_ops) w->n_scatter += (o.kind == 0);
   if ((rc = upload(w->ents, &w->d_ents)) || (rc = upload(w->pairs, &w->d_pairs)) ||
-      (rc = upload(w->reset_ops, &w->d_reset_ops))) {
+      (rc = upload(w->reset_ops, &w->d_reset_ops)) || (rc = upload(w->joints, &w->d_joints))) {
     free_world(w);
     return rc;
   }
@@ -144,6 +158,7 @@ int ss_world_create(const SsWorldDesc* desc, void** out_world) {
   w->d.pairs = nullptr;
   w->d.reset_ops = nullptr;
   w->d.lidar_dirs = nullptr;
+  w->d.joints = nullptr;
   *out_world = w;
   return SS_OK;
 }
@@ -160,6 +175,10 @@ int ss_env_step(void* world, const SsBuffers* buf, const SsStepIO* io, void* str
     set_error("actions required for a physics step"); return SS_ERR_CONTRACT;
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if ((io->mode & SS_DO_PHYSICS) && w->d.n_joints > 0 && w->d.scenario != SS_SCN_PHYSICS_ONLY) {
+    set_error("worlds with joints step their physics through ss_world_step (generic kernel)");
+    return SS_ERR_CONTRACT;
+  }
   switch (w->d.scenario) {
     case SS_SCN_SIMPLE_SPREAD:
     case SS_SCN_TRANSPORT:
@@ -181,12 +200,14 @@ int ss_env_step(void* world, const SsBuffers* buf, const SsStepIO* io, void* str
 }
 
 int ss_world_step(void* world, const SsBuffers* buf, const float* const* forces,
-                  const uint64_t* decode_mask, int32_t count, int32_t* d_status, void* stream) {
+                  const uint64_t* decode_mask, int32_t count, const int32_t* guard,
+                  int32_t* d_status, void* stream) {
   World* w = static_cast<World*>(world);
   if (!w || !buf) { set_error("null argument"); return SS_ERR_CONTRACT; }
   SsStepIO io;
   memset(&io, 0, sizeof(io));
   io.actions = forces;
+  io.guard = guard;
   io.mode = SS_DO_PHYSICS | (count ? SS_DO_COUNT : 0);
   return launch_generic(*w, buf, &io, decode_mask, d_status, static_cast<cudaStream_t>(stream));
 }

@@ -18,7 +18,9 @@ struct World {
   std::vector<SsEntityDesc> ents;
   std::vector<SsPairDesc> pairs;
   std::vector<SsResetOp> reset_ops;
+  std::vector<SsJointDesc> joints;
   SsEntityDesc* d_ents = nullptr;      // device copies
+  SsJointDesc* d_joints = nullptr;
   SsPairDesc* d_pairs = nullptr;
   SsResetOp* d_reset_ops = nullptr;
   double* d_lidar_dirs = nullptr;      // [lidar_rays][2]
@@ -65,8 +67,9 @@ inline DevState make_state(const World& w, const SsBuffers* b) {
 
 // Physics constants shared by every step kernel.
 struct PhysK {
-  float dt, keep, ck, k;
+  float dt, keep, ck, k;   // dt: the SUB-step f32(dt / substeps)
   int has_gravity;
+  int substeps;            // physics sub-steps per Env.step (1 = reference)
   int64_t max_steps;
 };
 
@@ -74,6 +77,7 @@ inline PhysK make_phys(const World& w) {
   PhysK p;
   p.dt = w.d.dt; p.keep = w.d.keep; p.ck = w.d.contact_ck; p.k = w.d.contact_k;
   p.has_gravity = w.d.has_gravity; p.max_steps = w.d.max_steps;
+  p.substeps = w.d.substeps > 0 ? w.d.substeps : 1;
   return p;
 }
 

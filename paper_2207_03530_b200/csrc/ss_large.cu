@@ -130,19 +130,25 @@ SS_DEV void agents_physics(const LargeArgs& a, float2* pos, float2* vel, int64_t
   }
   __syncwarp();
   if (a.mode & SS_DO_PHYSICS) {
-    float fx[T], fy[T];
+    float ux[T], uy[T];
 #pragma unroll
     for (int t = 0; t < T; ++t) {
       const int k = lane + 32 * t;
-      fx[t] = 0.0f; fy[t] = 0.0f;
+      ux[t] = 0.0f; uy[t] = 0.0f;
       if (k < a.NA) {
         const SsEntityDesc& d = a.ents[k];
         const float2 u = a.act[k][e];
-        fx[t] = a.raw_forces ? u.x : fmul(clip_sym(u.x, d.u_range), d.u_mult);
-        fy[t] = a.raw_forces ? u.y : fmul(clip_sym(u.y, d.u_range), d.u_mult);
-        if (a.ph.has_gravity) { fx[t] = fadd(fx[t], d.grav_x); fy[t] = fadd(fy[t], d.grav_y); }
+        ux[t] = a.raw_forces ? u.x : fmul(clip_sym(u.x, d.u_range), d.u_mult);
+        uy[t] = a.raw_forces ? u.y : fmul(clip_sym(u.y, d.u_range), d.u_mult);
+        if (a.ph.has_gravity) { ux[t] = fadd(ux[t], d.grav_x); uy[t] = fadd(uy[t], d.grav_y); }
       }
     }
+    // physics sub-steps (PhysK.substeps, 1 = reference): decoded actions held,
+    // contacts re-evaluated on the sub-step positions staged in pos[]
+    for (int sub = 0; sub < a.ph.substeps; ++sub) {
+    float fx[T], fy[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) { fx[t] = ux[t]; fy[t] = uy[t]; }
     if (PAIRS && masks != nullptr && a.NA <= 64) {
       // Contact bitmap.  The squared distance is symmetric (a - b == -(b - a)
       // and (-x)^2 == x^2 bitwise), so each unordered pair is tested once:
@@ -239,9 +245,15 @@ SS_DEV void agents_physics(const LargeArgs& a, float2* pos, float2* vel, int64_t
         const SsEntityDesc& d = a.ents[k];
         integrate_lin(px[t], py[t], vx[t], vy[t], fx[t], fy[t], a.ph.keep, d.inv_m_dt, a.ph.dt,
                       d.max_speed);
-        a.s.dyn[k * B + e] = make_float4(px[t], py[t], vx[t], vy[t]);
         pos[k] = make_float2(px[t], py[t]);
       }
+    }
+    __syncwarp();   // sub-step positions staged before the next sub-step reads them
+    }
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const int k = lane + 32 * t;
+      if (k < a.NA) a.s.dyn[k * B + e] = make_float4(px[t], py[t], vx[t], vy[t]);
     }
   }
 #pragma unroll

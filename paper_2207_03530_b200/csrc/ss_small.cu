@@ -132,34 +132,40 @@ struct SpreadEnv {
   static constexpr int O = 4 * NA + 2;
   float px[NA], py[NA], vx[NA], vy[NA], mx[NA], my[NA];
 
-  // decode + contacts (lexicographic pair order) + integrate
+  // decode + contacts (lexicographic pair order) + integrate, once per
+  // physics sub-step (PhysK.substeps; the decoded actions are held)
   SS_DEV void physics(const float2 (&u)[NA], const SmallArgs& a) {
-    float fx[NA], fy[NA];
+    float ux[NA], uy[NA];
 #pragma unroll
     for (int i = 0; i < NA; ++i) {
       const SsEntityDesc& d = a.ents[i];
-      fx[i] = decode_axis(u[i].x, d, a.raw_forces);
-      fy[i] = decode_axis(u[i].y, d, a.raw_forces);
-      if (a.ph.has_gravity) { fx[i] = fadd(fx[i], d.grav_x); fy[i] = fadd(fy[i], d.grav_y); }
+      ux[i] = decode_axis(u[i].x, d, a.raw_forces);
+      uy[i] = decode_axis(u[i].y, d, a.raw_forces);
+      if (a.ph.has_gravity) { ux[i] = fadd(ux[i], d.grav_x); uy[i] = fadd(uy[i], d.grav_y); }
     }
-    int p = 0;
+    for (int sub = 0; sub < a.ph.substeps; ++sub) {
+      float fx[NA], fy[NA];
 #pragma unroll
-    for (int i = 0; i < NA; ++i) {
+      for (int i = 0; i < NA; ++i) { fx[i] = ux[i]; fy[i] = uy[i]; }
+      int p = 0;
 #pragma unroll
-      for (int j = i + 1; j < NA; ++j, ++p) {
-        const SsPairDesc pr = a.pairs[p];
-        float cx, cy;
-        if (contact_force(px[i], py[i], px[j], py[j], pr.d_min, pr.d2_act, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
-          fx[i] = fadd(fx[i], cx); fy[i] = fadd(fy[i], cy);
-          fx[j] = fsub(fx[j], cx); fy[j] = fsub(fy[j], cy);
+      for (int i = 0; i < NA; ++i) {
+#pragma unroll
+        for (int j = i + 1; j < NA; ++j, ++p) {
+          const SsPairDesc pr = a.pairs[p];
+          float cx, cy;
+          if (contact_force(px[i], py[i], px[j], py[j], pr.d_min, pr.d2_act, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
+            fx[i] = fadd(fx[i], cx); fy[i] = fadd(fy[i], cy);
+            fx[j] = fsub(fx[j], cx); fy[j] = fsub(fy[j], cy);
+          }
         }
       }
-    }
 #pragma unroll
-    for (int i = 0; i < NA; ++i) {
-      const SsEntityDesc& d = a.ents[i];
-      integrate_lin(px[i], py[i], vx[i], vy[i], fx[i], fy[i], a.ph.keep, d.inv_m_dt, a.ph.dt,
-                    d.max_speed);
+      for (int i = 0; i < NA; ++i) {
+        const SsEntityDesc& d = a.ents[i];
+        integrate_lin(px[i], py[i], vx[i], vy[i], fx[i], fy[i], a.ph.keep, d.inv_m_dt, a.ph.dt,
+                      d.max_speed);
+      }
     }
   }
 
@@ -411,49 +417,55 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_transport(cons
     float ca, sa;
     if (prot == 0.0f) { ca = 1.0f; sa = prot; } else { ca = np_cosf(prot); sa = np_sinf(prot); }
     const double hx = a.sd[0], hy = a.sd[1];
-    float fx[NA + 1], fy[NA + 1];
+    float ux[NA + 1], uy[NA + 1];
 #pragma unroll
     for (int i = 0; i < NA; ++i) {
       const SsEntityDesc& d = a.ents[i];
-      fx[i] = decode_axis(u[i].x, d, a.raw_forces);
-      fy[i] = decode_axis(u[i].y, d, a.raw_forces);
+      ux[i] = decode_axis(u[i].x, d, a.raw_forces);
+      uy[i] = decode_axis(u[i].y, d, a.raw_forces);
     }
-    fx[NA] = 0.0f; fy[NA] = 0.0f;
+    ux[NA] = 0.0f; uy[NA] = 0.0f;
     if (a.ph.has_gravity) {
 #pragma unroll
       for (int i = 0; i <= NA; ++i) {
-        fx[i] = fadd(fx[i], a.ents[i].grav_x); fy[i] = fadd(fy[i], a.ents[i].grav_y);
+        ux[i] = fadd(ux[i], a.ents[i].grav_x); uy[i] = fadd(uy[i], a.ents[i].grav_y);
       }
     }
-    int p = 0;
+    for (int sub = 0; sub < a.ph.substeps; ++sub) {   // physics sub-steps (1 = reference)
+      float fx[NA + 1], fy[NA + 1];
 #pragma unroll
-    for (int i = 0; i < NA; ++i) {
+      for (int i = 0; i <= NA; ++i) { fx[i] = ux[i]; fy[i] = uy[i]; }
+      int p = 0;
 #pragma unroll
-      for (int j = i + 1; j < NA; ++j, ++p) {
-        const SsPairDesc pr = a.pairs[p];
-        float cx, cy;
-        if (contact_force(px[i], py[i], px[j], py[j], pr.d_min, pr.d2_act, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
-          fx[i] = fadd(fx[i], cx); fy[i] = fadd(fy[i], cy);
-          fx[j] = fsub(fx[j], cx); fy[j] = fsub(fy[j], cy);
+      for (int i = 0; i < NA; ++i) {
+#pragma unroll
+        for (int j = i + 1; j < NA; ++j, ++p) {
+          const SsPairDesc pr = a.pairs[p];
+          float cx, cy;
+          if (contact_force(px[i], py[i], px[j], py[j], pr.d_min, pr.d2_act, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
+            fx[i] = fadd(fx[i], cx); fy[i] = fadd(fy[i], cy);
+            fx[j] = fsub(fx[j], cx); fy[j] = fsub(fy[j], cy);
+          }
+        }
+        {  // agent i vs package (sphere-box)
+          const SsPairDesc pr = a.pairs[p++];
+          float qx, qy, cx, cy;
+          closest_point_on_box(px[i], py[i], px[NA], py[NA], ca, sa, hx, hy, qx, qy);
+          if (contact_force(px[i], py[i], qx, qy, pr.d_min, pr.d2_act, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
+            fx[i] = fadd(fx[i], cx); fy[i] = fadd(fy[i], cy);
+            fx[NA] = fsub(fx[NA], cx); fy[NA] = fsub(fy[NA], cy);
+          }
         }
       }
-      {  // agent i vs package (sphere-box)
-        const SsPairDesc pr = a.pairs[p++];
-        float qx, qy, cx, cy;
-        closest_point_on_box(px[i], py[i], px[NA], py[NA], ca, sa, hx, hy, qx, qy);
-        if (contact_force(px[i], py[i], qx, qy, pr.d_min, pr.d2_act, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
-          fx[i] = fadd(fx[i], cx); fy[i] = fadd(fy[i], cy);
-          fx[NA] = fsub(fx[NA], cx); fy[NA] = fsub(fy[NA], cy);
-        }
+#pragma unroll
+      for (int i = 0; i <= NA; ++i) {
+        const SsEntityDesc& d = a.ents[i];
+        integrate_lin(px[i], py[i], vx[i], vy[i], fx[i], fy[i], a.ph.keep, d.inv_m_dt, a.ph.dt,
+                      d.max_speed);
       }
     }
 #pragma unroll
-    for (int i = 0; i <= NA; ++i) {
-      const SsEntityDesc& d = a.ents[i];
-      integrate_lin(px[i], py[i], vx[i], vy[i], fx[i], fy[i], a.ph.keep, d.inv_m_dt, a.ph.dt,
-                    d.max_speed);
-      a.s.dyn[i * B + e] = make_float4(px[i], py[i], vx[i], vy[i]);
-    }
+    for (int i = 0; i <= NA; ++i) a.s.dyn[i * B + e] = make_float4(px[i], py[i], vx[i], vy[i]);
   }
   if (valid && (a.mode & SS_DO_COUNT)) { steps += 1; a.s.step_count[e] = steps; }
   if (valid && (a.mode & (SS_DO_REWARD | SS_DO_DONE))) {
@@ -539,7 +551,8 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_dropout(const 
       float fx = decode_axis(u[i].x, d, a.raw_forces), fy = decode_axis(u[i].y, d, a.raw_forces);
       spent = dadd_rn(dadd_rn(spent, (double)fmul(fx, fx)), (double)fmul(fy, fy));
       if (a.ph.has_gravity) { fx = fadd(fx, d.grav_x); fy = fadd(fy, d.grav_y); }
-      integrate_lin(px[i], py[i], vx[i], vy[i], fx, fy, a.ph.keep, d.inv_m_dt, a.ph.dt, d.max_speed);
+      for (int sub = 0; sub < a.ph.substeps; ++sub)   // no pairs: sub-steps are independent
+        integrate_lin(px[i], py[i], vx[i], vy[i], fx, fy, a.ph.keep, d.inv_m_dt, a.ph.dt, d.max_speed);
       a.s.dyn[i * B + e] = make_float4(px[i], py[i], vx[i], vy[i]);
     }
     a.s.flags[e] = (uint32_t)__double2loint(spent);
@@ -1272,15 +1285,19 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_flocking(const
     }
   }
   if (valid && (a.mode & SS_DO_PHYSICS)) {
-    float fx[NA], fy[NA];
+    float ux[NA], uy[NA];
 #pragma unroll
     for (int i = 0; i < NA; ++i) {
       const SsEntityDesc& d = a.ents[i];
       const float2 u = a.act[i][e];
-      fx[i] = decode_axis(u.x, d, a.raw_forces);
-      fy[i] = decode_axis(u.y, d, a.raw_forces);
-      if (a.ph.has_gravity) { fx[i] = fadd(fx[i], d.grav_x); fy[i] = fadd(fy[i], d.grav_y); }
+      ux[i] = decode_axis(u.x, d, a.raw_forces);
+      uy[i] = decode_axis(u.y, d, a.raw_forces);
+      if (a.ph.has_gravity) { ux[i] = fadd(ux[i], d.grav_x); uy[i] = fadd(uy[i], d.grav_y); }
     }
+    for (int sub = 0; sub < a.ph.substeps; ++sub) {   // physics sub-steps (1 = reference)
+    float fx[NA], fy[NA];
+#pragma unroll
+    for (int i = 0; i < NA; ++i) { fx[i] = ux[i]; fy[i] = uy[i]; }
     int p = 0;
 #pragma unroll
     for (int i = 0; i < NA; ++i) {
@@ -1309,8 +1326,10 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_flocking(const
       const SsEntityDesc& d = a.ents[i];
       integrate_lin(px[i], py[i], vx[i], vy[i], fx[i], fy[i], a.ph.keep, d.inv_m_dt, a.ph.dt,
                     d.max_speed);
-      a.s.dyn[i * B + e] = make_float4(px[i], py[i], vx[i], vy[i]);
     }
+    }
+#pragma unroll
+    for (int i = 0; i < NA; ++i) a.s.dyn[i * B + e] = make_float4(px[i], py[i], vx[i], vy[i]);
   }
   int64_t steps = 0;
   if (valid && (a.mode & (SS_DO_COUNT | SS_DO_DONE))) {
@@ -1468,11 +1487,19 @@ __global__ void __launch_bounds__(32 * NA, (SS_FLOCK_WARPS / NA < 32 ? SS_FLOCK_
     for (int k = i; k < 1 + NO; k += NA) sst[k * 32 + lane] = a.s.stat[k * B + e];
   }
   __syncthreads();
-  if (valid && (a.mode & SS_DO_PHYSICS)) {
+  if (a.mode & SS_DO_PHYSICS) {
     const SsEntityDesc& d = a.ents[i];
-    float fx = decode_axis(u.x, d, a.raw_forces), fy = decode_axis(u.y, d, a.raw_forces);
-    if (a.ph.has_gravity) { fx = fadd(fx, d.grav_x); fy = fadd(fy, d.grav_y); }
+    float ux = decode_axis(u.x, d, a.raw_forces), uy = decode_axis(u.y, d, a.raw_forces);
+    if (a.ph.has_gravity) { ux = fadd(ux, d.grav_x); uy = fadd(uy, d.grav_y); }
     const float dmin_aa = a.sc[5], d2_aa = a.sc[6], dmin_ar = a.sc[7], d2_ar = a.sc[8];
+    for (int sub = 0; sub < a.ph.substeps; ++sub) {   // physics sub-steps (1 = reference)
+    if (sub > 0) {   // restage every agent's sub-step state (all threads reach both barriers)
+      __syncthreads();
+      if (valid) sag[i * 32 + lane] = me;
+      __syncthreads();
+    }
+    if (valid) {
+    float fx = ux, fy = uy;
 #pragma unroll
     for (int j = 0; j < NA; ++j) {
       if (j == i) continue;
@@ -1498,7 +1525,9 @@ __global__ void __launch_bounds__(32 * NA, (SS_FLOCK_WARPS / NA < 32 ? SS_FLOCK_
       }
     }
     integrate_lin(me.x, me.y, me.z, me.w, fx, fy, a.ph.keep, d.inv_m_dt, a.ph.dt, d.max_speed);
-    a.s.dyn[i * B + e] = me;
+    }
+    }
+    if (valid) a.s.dyn[i * B + e] = me;
   }
   if (valid) spos[i * 32 + lane] = make_float2(me.x, me.y);
   __syncthreads();                       // post-step positions of every agent staged

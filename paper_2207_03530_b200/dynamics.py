@@ -92,11 +92,14 @@ def physics_world(world: World):
     return world.native(("physics", world.version), lambda: world.base_desc())
 
 
-def run_world_step(world: World, forces: list, decode_mask: int, count: bool, stream=None) -> None:
+def run_world_step(world: World, forces: list, decode_mask: int, count: bool, stream=None,
+                   guard=None) -> None:
     """Launch the generic step kernel.
 
     forces[a]: agent a's (B, 2) f32 device tensor, or its data pointer (int).
     decode_mask bit a: apply decode_action's clip * u_multiplier on device.
+    guard: optional (1,) int32 device flag from ss_check_actions; a nonzero
+    flag (NaN action) turns the launch into a no-op (env.py:85: nothing moves).
     """
     h = physics_world(world)
     ptrs = (ctypes.c_void_p * max(1, len(forces)))()
@@ -105,7 +108,8 @@ def run_world_step(world: World, forces: list, decode_mask: int, count: bool, st
     mask = (ctypes.c_uint64 * 4)(*[(decode_mask >> (64 * i)) & (2**64 - 1) for i in range(4)])
     status = torch.zeros(1, dtype=torch.int32, device=world.device)
     st = stream if stream is not None else N.stream_handle(world.device)
-    N.check(N.lib().ss_world_step(h.handle, world.buffers_ref(), ptrs, mask, int(count), N.ptr(status), st))
+    N.check(N.lib().ss_world_step(h.handle, world.buffers_ref(), ptrs, mask, int(count), N.ptr(guard),
+                                  N.ptr(status), st))
 
 
 def world_step(world: World, actions: list) -> None:

@@ -14,7 +14,7 @@ from __future__ import annotations
 
 import gc
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, replace
 
 import numpy as np
 import torch
@@ -147,7 +147,7 @@ class Env:
 
     def __init__(self, scenario: Scenario, batch_size: int, seed: int = 0, max_steps: int | None = None,
                  action_mode: str = "continuous", device=None, validate: bool = True,
-                 env_offset: int = 0, global_batch: int | None = None):
+                 env_offset: int = 0, global_batch: int | None = None, substeps: int | None = None):
         if batch_size < 1:
             raise ContractViolation(f"batch_size must be >= 1, got {batch_size}")
         if action_mode not in ("continuous", "discrete"):
@@ -166,9 +166,18 @@ class Env:
             self.rng = DeviceRng(seed, dev)
             self.world = _make_world(scenario, batch_size, self.rng, dev)
         self.world.rng = self.rng
+        if substeps is not None:
+            # extension: physics sub-steps per step (PhysParams.substeps)
+            self.world.params = replace(self.world.params, substeps=substeps)
         gb = self.batch_size if global_batch is None else int(global_batch)
         if env_offset < 0 or env_offset + self.batch_size > gb:
             raise ContractViolation("shard [env_offset, env_offset + batch_size) outside global_batch")
+        if (env_offset != 0 or gb != self.batch_size) and not getattr(scenario, "shardable_reset", False):
+            # a host reset program draws B values from the stream, not the
+            # shard's slice of the global batch: a sharded run would give
+            # every shard rank 0's initial states
+            raise ContractViolation(f"{type(scenario).__name__} resets on the host: it cannot run as a "
+                                    "shard (env_offset / global_batch) of a larger batch")
         self.world.env_offset = int(env_offset)
         self.world.global_batch = gb
         self.world._touch()
@@ -351,18 +360,36 @@ class Env:
             infos = [sc.info(a, world) for a in self.agents]
         return StepResult(obs=obs_list, rewards=list(rew.unbind(0)), dones=done, infos=infos)
 
-    def _capture_step(self, ptrs, keepalive) -> StepResult:
-        """One fused step without validation or host syncs (graph capture)."""
+    def _capture_step(self, ptrs, keepalive, flag=None) -> StepResult:
+        """One fused step without host syncs (graph capture).  flag: a device
+        int32 the step's NaN scan ORs into; a set flag makes the launch a
+        no-op (the guard of the eager validated step, left for the host to
+        read after the replay instead of syncing inside it)."""
         saved = self.validate
         self.validate = False
         try:
-            return self._step_fused_ptrs(ptrs, keepalive, False)
+            if flag is None:
+                return self._step_fused_ptrs(ptrs, keepalive, False)
+            st = torch.cuda.current_stream(self.device).cuda_stream
+            h = self.scenario.native_handle(self.world)
+            arr = (N.c_vp * max(1, len(ptrs)))(*ptrs)
+            N.check(N.lib().ss_check_actions(h.handle, arr, flag.data_ptr(), st))
+            obs, rew, done = self.scenario.launch(self.world, N.MODE_STEP, action_ptrs=ptrs, guard=flag,
+                                                  flip_rng=False, stream=st)
+            B = self.batch_size
+            obs_list = list((obs if obs.shape[1] == B else obs[:, :B]).unbind(0))
+            return StepResult(obs=obs_list, rewards=list(rew.unbind(0)), dones=done,
+                              infos=[{} for _ in self.agents])
         finally:
             self.validate = saved
 
-    def step_graph(self, actions, steps_per_replay: int = 1) -> "StepGraph":
-        """Capture Env.step into CUDA graphs over the given action buffer(s)."""
-        return StepGraph(self, actions, steps_per_replay)
+    def step_graph(self, actions, steps_per_replay: int = 1, validate: bool = False) -> "StepGraph":
+        """Capture Env.step into CUDA graphs over the given action buffer(s).
+
+        validate=True keeps the reference's NaN check inside the graph: each
+        step scans its actions and is a no-op once any NaN was seen in the
+        replay; StepGraph.check() raises ContractViolation afterwards."""
+        return StepGraph(self, actions, steps_per_replay, validate)
 
     @property
     def _any_obs_noise(self) -> bool:
@@ -407,7 +434,7 @@ class StepGraph:
     (discovery) get one graph per half of the double-buffered Philox state.
     """
 
-    def __init__(self, env: Env, actions, steps_per_replay: int = 1):
+    def __init__(self, env: Env, actions, steps_per_replay: int = 1, validate: bool = False):
         acts = [actions] if isinstance(actions, torch.Tensor) else list(actions)
         A, B = len(env.agents), env.batch_size
         S = int(steps_per_replay)
@@ -426,6 +453,10 @@ class StepGraph:
         # scripted agents (or a non-fused scenario): capture the whole public
         # step — scripts, decode, launches — instead of the bare fused launch
         self._generic = not env.fused or env._needs_host_decode([0] * A)
+        if validate and self._generic:
+            raise ContractViolation("StepGraph(validate=True) covers the fused built-in step")
+        # NaN verdict of the replay (validate=True), zeroed at its start
+        self.nan_flag = torch.zeros(1, dtype=torch.int32, device=env.device) if validate else None
         sc, world = env.scenario, env.world
         self._rng_mode = bool(getattr(sc, "advances_rng_per_step", False))
         world.ensure_device_rng()
@@ -462,6 +493,10 @@ class StepGraph:
             world.rng.capture_guard = False
         torch.cuda.current_stream(env.device).wait_stream(stream)
         world.rng.cur = start_cur
+        self._start_cur = start_cur
+        # the captured kernels hold this world's descriptor tables and state
+        # buffers: any later edit that rebuilds them retires the graph
+        self._epoch = (world.native_epoch, world.version, world.rng)
 
     def _capture_all(self, env, acts, A, B, S, start_cur, stream) -> None:
         world = env.world
@@ -471,13 +506,16 @@ class StepGraph:
                 g = torch.cuda.CUDAGraph()
                 results = []
                 with torch.cuda.stream(stream), torch.cuda.graph(g, stream=stream):
+                    if self.nan_flag is not None:
+                        self.nan_flag.zero_()
                     for k in range(S):
                         act = acts[(i + k) % len(acts)]
                         if self._generic:
                             results.append(self._capture_generic(act))
                             continue
                         base, stride = act.data_ptr(), B * 8
-                        results.append(env._capture_step([base + a * stride for a in range(A)], act))
+                        results.append(env._capture_step([base + a * stride for a in range(A)], act,
+                                                         self.nan_flag))
                 self._graphs[(cur, i)] = g
                 self._results[(cur, i)] = results
 
@@ -494,8 +532,14 @@ class StepGraph:
             rng.capture_guard = False
 
     def _replay(self, i: int) -> list:
-        rng = self.env.world.rng
-        key = (rng.cur, i)
+        world = self.env.world
+        if (world.native_epoch, world.version, world.rng) != self._epoch:
+            raise ContractViolation("the world was edited since this StepGraph was captured "
+                                    "(its descriptor / buffers were rebuilt): capture a new one")
+        rng = world.rng
+        # rng-mode scenarios have one graph per Philox half; the others one
+        # graph whatever the current half (a reset flips it between replays)
+        key = (rng.cur if self._rng_mode else self._start_cur, i)
         self._graphs[key].replay()
         if self._rng_mode and self.steps_per_replay % 2:
             rng.flip()
@@ -504,6 +548,12 @@ class StepGraph:
     def step(self, i: int = 0) -> StepResult:
         """Replay graph i; returns the outputs of its last step."""
         return self._replay(i)[-1]
+
+    def check(self) -> None:
+        """validate=True: raise ContractViolation if the last replay met a NaN
+        action (the steps from that one on did not move anything).  Syncs."""
+        if self.nan_flag is not None and int(self.nan_flag.item()) != 0:
+            raise ContractViolation("an action replayed by this StepGraph contains NaN")
 
     def rollout(self, i: int = 0) -> list:
         """Replay graph i; returns the S StepResults of its steps, in order."""
@@ -520,16 +570,20 @@ def _make_world(scenario: Scenario, batch_size: int, rng, device) -> World:
 def _as_mask(mask, B: int, device) -> torch.Tensor:
     if isinstance(mask, (int, np.integer)):
         idx = [int(mask)]
-    elif isinstance(mask, torch.Tensor) and mask.dtype == torch.bool:
+    elif isinstance(mask, torch.Tensor) and mask.dtype in (torch.bool, torch.uint8):
+        # a (B,) bool or uint8 tensor is a mask (dones.to(torch.uint8) included)
         if tuple(mask.shape) != (B,):
             raise ContractViolation(f"reset mask must have shape ({B},), got {tuple(mask.shape)}")
-        return mask.to(device)
+        return mask.to(device) != 0
     else:
         arr = np.asarray(mask.cpu() if isinstance(mask, torch.Tensor) else mask)
-        if arr.dtype == bool:
+        if arr.dtype == bool or arr.dtype == np.uint8:
             if arr.shape != (B,):
                 raise ContractViolation(f"reset mask must have shape ({B},), got {arr.shape}")
-            return torch.from_numpy(arr).to(device)
+            return torch.from_numpy(arr != 0).to(device)
+        if arr.ndim == 1 and arr.shape == (B,) and B > 2 and np.isin(arr, (0, 1)).all():
+            raise ContractViolation("ambiguous reset selector: a (B,) array of 0/1 integers; pass a bool "
+                                    "mask or an explicit index list")
         idx = [int(i) for i in arr.reshape(-1)]
     for i in idx:
         if not (0 <= i < B):
@@ -570,11 +624,12 @@ class SingleEnv:
 
 
 def make_env(scenario, num_envs: int = 32, device=None, continuous_actions: bool = True,
-             max_steps: int | None = None, seed: int | None = None, validate: bool = True, **kwargs) -> Env:
+             max_steps: int | None = None, seed: int | None = None, validate: bool = True,
+             substeps: int | None = None, **kwargs) -> Env:
     """VMAS-style constructor: make_env("simple_spread", num_envs=1_000_000, n_agents=3)."""
     from .scenarios import create_scenario
 
     sc = create_scenario(scenario, **kwargs) if isinstance(scenario, str) else scenario
     return Env(sc, num_envs, seed=0 if seed is None else seed, max_steps=max_steps,
                action_mode="continuous" if continuous_actions else "discrete", device=device,
-               validate=validate)
+               validate=validate, substeps=substeps)

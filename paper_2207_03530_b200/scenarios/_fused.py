@@ -28,6 +28,7 @@ from ..env import Scenario
 class FusedScenario(Scenario):
     native_id: int | None = None
     advances_rng_per_step = False   # discovery draws relocations every step
+    shardable_reset = True          # the device reset draws at global env indices
 
     # ---- subclass interface -------------------------------------------------
     def obs_dim(self, world: World) -> int:
@@ -51,8 +52,10 @@ class FusedScenario(Scenario):
         return True
 
     # ---- descriptor ---------------------------------------------------------
-    def native_desc(self, world: World) -> "N.SsWorldDesc":
-        d = world.base_desc(self.native_id, getattr(world, "max_steps", self.max_steps))
+    def native_desc(self, world: World, max_steps: int | None = None) -> "N.SsWorldDesc":
+        if max_steps is None:
+            max_steps = getattr(world, "max_steps", self.max_steps)
+        d = world.base_desc(self.native_id, max_steps)
         d.obs_dim = self.obs_dim(world)
         d.n_flag_words = world.flags.shape[0]
         ops = self.reset_ops(world)
@@ -75,15 +78,19 @@ class FusedScenario(Scenario):
         d._keep = (d._keep, arr)
         return d
 
-    def native_handle(self, world: World):
+    def native_handle(self, world: World, horizon: bool = True):
+        """Cached SsWorld of this world version; horizon=False: the same world
+        without the step horizon (the scenario's own done term only)."""
         world.ensure_flag_words(self.n_flag_words())
-        return world.native(("fused", world.version), lambda: self.native_desc(world))
+        if horizon:
+            return world.native(("fused", world.version), lambda: self.native_desc(world))
+        return world.native(("fused-nohorizon", world.version), lambda: self.native_desc(world, 2**62))
 
     def physics_fused(self, world: World) -> bool:
         key = ("tmpl", world.version)
         ok = world._native_cache.get(key)
         if ok is None:
-            ok = _Flag(self.template_ok(world) and
+            ok = _Flag(self.template_ok(world) and not world.joints and
                        list(world.collidable_pairs()) == list(self.template_pairs(world)))
             world._native_cache[key] = ok
         return ok.value
@@ -102,20 +109,20 @@ class FusedScenario(Scenario):
         return obs, rew, done
 
     def launch(self, world: World, mode: int, action_ptrs=None, raw_forces: bool = False,
-               guard=None, flip_rng: bool = True, stream: int | None = None):
+               guard=None, flip_rng: bool = True, stream: int | None = None, horizon: bool = True):
         """One fused launch in `mode`; returns (obs (A, Bp, O), rew (A, B), done (B,)).
 
         action_ptrs: one device pointer per agent to a contiguous (B, 2) f32
         block (the caller keeps the tensors alive until the launch is queued).
         """
         world.ensure_device_rng()
-        h = self.native_handle(world)
+        h = self.native_handle(world, horizon)
         st = stream if stream is not None else N.stream_handle(world.device)
         if (mode & N.DO_PHYSICS) and not self.physics_fused(world):
             from ..dynamics import run_world_step
 
             run_world_step(world, action_ptrs, decode_mask=0 if raw_forces else (1 << 256) - 1,
-                           count=False, stream=st)
+                           count=False, stream=st, guard=guard)
             mode &= ~N.DO_PHYSICS
         obs, rew, done = self.alloc_outputs(world, h.obs_dim)
         io = h.io
@@ -147,15 +154,10 @@ class FusedScenario(Scenario):
         return rew[world.agents.index(agent)]
 
     def done(self, world: World) -> torch.Tensor:
-        # scenario termination only: the horizon term is Env's (env.py:232)
-        saved = getattr(world, "max_steps", self.max_steps)
-        try:
-            world.max_steps = 2**62
-            world._drop_native()
-            _, _, done = self.launch(world, N.DO_DONE)
-        finally:
-            world.max_steps = saved
-            world._drop_native()
+        # scenario termination only: the horizon term is Env's (env.py:232);
+        # a second cached descriptor without the horizon, so no live handle
+        # (and no captured StepGraph) is ever freed by this hook
+        _, _, done = self.launch(world, N.DO_DONE, horizon=False)
         return done
 
     def post_step(self, world: World) -> None:
@@ -187,6 +189,7 @@ class HostReset:
     Env's Philox stream), one env at a time, ascending, for masked resets."""
 
     _reference: type = None
+    shardable_reset = False
 
     def reset_ops(self, world):
         return []

@@ -1,0 +1,107 @@
+"""Contract edge cases of the device Env: CUDA-graph stepping across resets
+and world edits, the NaN guard on every physics path, shard refusal for host
+reset programs, and reset-selector parsing (env.py:85, 189-198 semantics)."""
+import numpy as np
+import pytest
+import torch
+
+import golden_util as G
+import paper_2207_03530_b200 as S
+
+pytestmark = pytest.mark.gpu
+
+
+def state(e):
+    return e.world.state_array().cpu().numpy()
+
+
+@pytest.mark.parametrize("name", ["simple_spread", "transport", "flocking", "dispersion", "discovery", "dropout"])
+def test_step_graph_survives_resets(cuda, name):
+    """replay, reset the done envs, replay: the usual RL loop, for every
+    reset-kernel scenario, bitwise equal to eager stepping."""
+    B = 96
+    a = S.Env(S.create_scenario(name), B, seed=3, device=cuda, validate=False)
+    b = S.Env(S.create_scenario(name), B, seed=3, device=cuda, validate=False)
+    A = len(a.agents)
+    g = torch.Generator(device=cuda)
+    g.manual_seed(5)
+    buf = torch.empty((A, B, 2), device=cuda)
+    graph = b.step_graph(buf)
+    mask = torch.zeros(B, dtype=torch.bool, device=cuda)
+    mask[::7] = True
+    for t in range(6):
+        buf.copy_(torch.rand((A, B, 2), device=cuda, generator=g) * 2 - 1)
+        ra = a.step(buf.clone())
+        rb = graph.step()
+        for x, y in zip(ra.obs + ra.rewards, rb.obs + rb.rewards):
+            assert torch.equal(x, y), f"step {t}"
+        assert torch.equal(ra.dones, rb.dones)
+        a.reset_at(mask)
+        b.reset_at(mask)
+        if t == 3:
+            a.reset()
+            b.reset()
+    np.testing.assert_array_equal(state(a), state(b))
+
+
+def test_step_graph_refuses_after_world_edit(cuda):
+    e = S.Env(S.create_scenario("simple_spread"), 64, seed=0, device=cuda, validate=False)
+    buf = torch.zeros((3, 64, 2), device=cuda)
+    graph = e.step_graph(buf)
+    graph.step()
+    e.scenario.done(e.world)          # a hook launch does not retire the graph
+    graph.step()
+    e.max_steps = 17                  # rebuilds the descriptor (new horizon)
+    with pytest.raises(S.ContractViolation, match="edited"):
+        graph.step()
+    e.step_graph(buf).step()          # a fresh capture works
+
+
+def test_done_hook_keeps_horizon_out(cuda):
+    e = S.Env(S.create_scenario("transport"), 8, seed=0, device=cuda, max_steps=1)
+    e.step([np.zeros((8, 2), np.float32)] * 4)
+    assert bool(e.step([np.zeros((8, 2), np.float32)] * 4).dones.all())     # horizon reached
+    assert not bool(e.scenario.done(e.world).any())                          # scenario term only
+
+
+@pytest.mark.parametrize("name", ["wheel", "balance", "waterfall", "give_way", "passage"])
+def test_nan_guard_on_generic_physics(cuda, name):
+    """The catalog tasks whose physics is world_step's generic kernel: a NaN
+    action must leave every buffer untouched, like the fused path."""
+    e = S.Env(S.create_scenario(name), 6, seed=2, device=cuda)
+    plan = G.pregen_actions(len(e.agents), 6, 2, 3)
+    e.step(plan[0])
+    before, steps = state(e), e.step_count.clone()
+    bad = [a.copy() for a in plan[1]]
+    bad[0][3, 1] = np.nan
+    with pytest.raises(S.ContractViolation, match="NaN"):
+        e.step(bad)
+    np.testing.assert_array_equal(state(e), before)
+    assert torch.equal(e.step_count, steps)
+
+
+@pytest.mark.parametrize("name", ["wheel", "football"])
+def test_host_reset_refuses_sharding(cuda, name):
+    sc = S.create_scenario(name)
+    if getattr(sc, "shardable_reset", False):
+        pytest.skip(f"{name} resets on the device")
+    with pytest.raises(S.ContractViolation, match="shard"):
+        S.Env(sc, 8, device=cuda, env_offset=8, global_batch=16)
+
+
+def test_reset_at_selectors(cuda):
+    B = 6
+    e = S.Env(S.create_scenario("simple_spread"), B, seed=1, device=cuda)
+    ref = S.Env(S.create_scenario("simple_spread"), B, seed=1, device=cuda)
+    for plan in G.pregen_actions(3, B, 3, 2):
+        e.step(plan)
+        ref.step(plan)
+    sel = torch.tensor([0, 1, 0, 0, 1, 0], device=cuda)
+    e.reset_at(sel.to(torch.uint8))                      # uint8 tensor is a mask
+    ref.reset_at(torch.tensor([False, True, False, False, True, False], device=cuda))
+    np.testing.assert_array_equal(state(e), state(ref))
+    e.reset_at(np.array([0, 1, 0, 0, 1, 0], dtype=np.uint8))
+    ref.reset_at([1, 4])                                  # explicit index list
+    np.testing.assert_array_equal(state(e), state(ref))
+    with pytest.raises(S.ContractViolation, match="ambiguous"):
+        e.reset_at(np.array([0, 1, 0, 0, 1, 0]))

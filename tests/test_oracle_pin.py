@@ -117,3 +117,67 @@ def test_oracle_lidar_matches_reference(reference):
     lid = reference.Lidar(n_rays=16, max_range=0.8)
     for i, agent in enumerate(ref.agents):
         np.testing.assert_array_equal(O.lidar(orc.ws, i, 16, 0.8), reference.lidar_scan(agent, lid, ref.world))
+
+
+def _ref_step_substeps(reference, env, plan, k):
+    """The reference's Env.step (env.py:209-235) with world_step replaced by k
+    reference world_step calls at PhysParams(dt=dt/k) on the held decoded
+    actions: the definition of the sub-step extension (core.PhysParams)."""
+    import dataclasses
+
+    from swarmsim.dynamics import world_step
+    from swarmsim.env import decode_action
+
+    actions = [decode_action(raw, spec, agent, env.rng) for raw, agent, spec in
+               zip(plan, env.agents, env.action_specs)]
+    base = env.world.params
+    env.world.params = dataclasses.replace(base, dt=base.dt / k)
+    try:
+        for _ in range(k):
+            world_step(env.world, actions)
+    finally:
+        env.world.params = base
+    env.scenario.post_step(env.world)
+    env.step_count += 1
+    rew = [env.scenario.reward(a, env.world).astype(np.float32) for a in env.agents]
+    done = env.scenario.done(env.world) | (env.step_count >= env.max_steps)
+    return env.observations(), rew, done
+
+
+@pytest.mark.reference
+@pytest.mark.parametrize("name,ov,k", [("simple_spread", {"n_agents": 3}, 4), ("transport", {"n_agents": 4}, 3),
+                                       ("flocking", {"n_agents": 5, "n_obstacles": 3}, 2),
+                                       ("discovery", {"n_agents": 6}, 3)])
+def test_oracle_substeps_match_reference_composition(reference, name, ov, k):
+    """Oracle with Phys.substeps = k == k reference world_step calls of dt / k
+    per step (pins the sub-step extension to the reference's own functions)."""
+    B, steps = 48, 25
+    ref = reference.Env(reference.create_scenario(name, **ov), batch_size=B, seed=5)
+    orc = O.OracleEnv(name, B, seed=5, substeps=k, **ov)
+    for t, plan in enumerate(G.pregen_actions(len(ref.agents), B, steps, 77)):
+        r_obs, r_rew, r_done = _ref_step_substeps(reference, ref, plan, k)
+        obs, rew, done = orc.step(plan)
+        np.testing.assert_array_equal(_state(orc), _ref_state(ref), err_msg=f"step {t}")
+        for a, b in zip(obs, r_obs):
+            np.testing.assert_array_equal(a, b)
+        for a, b in zip(rew, r_rew):
+            np.testing.assert_array_equal(a, b)
+        np.testing.assert_array_equal(done, r_done)
+
+
+def test_oracle_joint_newton_and_pull():
+    """Joint forces are equal and opposite (bitwise) and pull a stretched
+    pair together / push a compressed pair apart."""
+    bodies = [O.Body("a", "sphere", (0.05,), movable=True), O.Body("b", "sphere", (0.05,), movable=True)]
+    ws = O.WorldState(bodies, 64)
+    rng = np.random.default_rng(0)
+    ws.px[0] = rng.uniform(-1, 1, 64).astype(np.float32)
+    ws.py[0] = rng.uniform(-1, 1, 64).astype(np.float32)
+    d0 = np.hypot(ws.px[0] - ws.px[1], ws.py[0] - ws.py[1])
+    O.world_step(ws, {}, joints=[O.JointSpec(0, 1, dist=0.5)])
+    np.testing.assert_array_equal(ws.vx[0], -ws.vx[1])
+    np.testing.assert_array_equal(ws.vy[0], -ws.vy[1])
+    d1 = np.hypot(ws.px[0] - ws.px[1], ws.py[0] - ws.py[1])
+    far, near = d0 > 0.51, d0 < 0.49
+    assert far.any() and near.any()
+    assert (d1[far] < d0[far]).all() and (d1[near] > d0[near]).all()
