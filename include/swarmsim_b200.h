@@ -189,9 +189,11 @@ typedef struct SsStepIO {
   float* rew;             /* [n_agents][B] */
   uint8_t* done;          /* [B] */
   int32_t mode;           /* SS_DO_* flags */
-  const int32_t* guard;   /* optional device flag: if *guard != 0 the launch is a no-op */
+  const int32_t* guard;   /* optional device flags: if any of guard[0 .. guard_count) is
+                             nonzero the launch is a no-op (the NaN verdict, env.py:85) */
   int32_t raw_forces;     /* nonzero: actions are final forces (discrete / noisy /
                              scripted agents decoded by the host); skip decode_action */
+  int32_t guard_count;    /* words at guard (0 means 1) */
 } SsStepIO;
 
 typedef struct SsLidarDesc {
@@ -267,11 +269,12 @@ int ss_closest_points(const float* pos_i /*[n][2]*/, const float* rot_i, int32_t
  * (4 x uint64, NULL = all) applies decode_action's clip*u_multiplier to it
  * (Env.step path) instead of using it as-is (AgentAction / action_script
  * path).  count != 0 also increments step_count.  guard (device, may be
- * NULL): if *guard != 0 the launch leaves every buffer untouched (the NaN
- * verdict of ss_check_actions, env.py:85).  *d_status as above. */
+ * NULL): if any of guard[0 .. guard_count) is nonzero the launch leaves every
+ * buffer untouched (the NaN verdict of ss_check_actions, env.py:85).
+ * *d_status as above. */
 int ss_world_step(void* world, const SsBuffers* buf, const float* const* forces,
                   const uint64_t* decode_mask, int32_t count, const int32_t* guard,
-                  int32_t* d_status, void* stream);
+                  int32_t guard_count, int32_t* d_status, void* stream);
 
 #ifdef __cplusplus
 }

@@ -18,9 +18,11 @@ int main(void) {
   Z(SsWorldDesc); F(SsWorldDesc, batch); F(SsWorldDesc, max_steps); F(SsWorldDesc, dt);
   F(SsWorldDesc, entities); F(SsWorldDesc, pairs); F(SsWorldDesc, reset_ops); F(SsWorldDesc, sc);
   F(SsWorldDesc, sd); F(SsWorldDesc, si); F(SsWorldDesc, lidar_rays); F(SsWorldDesc, lidar_max_range);
-  F(SsWorldDesc, lidar_dirs);
+  F(SsWorldDesc, lidar_dirs); F(SsWorldDesc, substeps); F(SsWorldDesc, n_joints); F(SsWorldDesc, joints);
+  Z(SsJointDesc); F(SsJointDesc, ox_a); F(SsJointDesc, dist); F(SsJointDesc, stiffness); F(SsJointDesc, rotate_b);
   Z(SsBuffers); F(SsBuffers, rng); F(SsBuffers, rng_cur);
   Z(SsStepIO); F(SsStepIO, obs_agent_stride); F(SsStepIO, mode); F(SsStepIO, guard); F(SsStepIO, raw_forces);
+  F(SsStepIO, guard_count);
   Z(SsLidarDesc); F(SsLidarDesc, max_range); F(SsLidarDesc, dir_table);
   printf("\"end\": 0}\n");
   return 0;

@@ -79,7 +79,7 @@ class SsBuffers(ctypes.Structure):
 class SsStepIO(ctypes.Structure):
     _fields_ = [("actions", ctypes.POINTER(c_vp)), ("obs", c_vp), ("obs_agent_stride", c_i64),
                 ("rew", c_vp), ("done", c_vp), ("mode", c_i32), ("guard", c_vp),
-                ("raw_forces", c_i32)]
+                ("raw_forces", c_i32), ("guard_count", c_i32)]
 
 
 class SsLidarDesc(ctypes.Structure):
@@ -97,7 +97,7 @@ def _declare(lib) -> None:
     lib.ss_world_create.argtypes = [P(SsWorldDesc), P(c_vp)]
     lib.ss_world_destroy.argtypes = [c_vp]
     lib.ss_env_step.argtypes = [c_vp, P(SsBuffers), P(SsStepIO), c_vp]
-    lib.ss_world_step.argtypes = [c_vp, P(SsBuffers), P(c_vp), P(ctypes.c_uint64), c_i32, c_vp, c_vp, c_vp]
+    lib.ss_world_step.argtypes = [c_vp, P(SsBuffers), P(c_vp), P(ctypes.c_uint64), c_i32, c_vp, c_i32, c_vp, c_vp]
     lib.ss_reset.argtypes = [c_vp, P(SsBuffers), c_vp, c_vp, c_vp, c_vp]
     lib.ss_mask_count.argtypes = [c_vp, c_vp, c_vp, c_vp]
     lib.ss_check_actions.argtypes = [c_vp, P(c_vp), c_vp, c_vp]

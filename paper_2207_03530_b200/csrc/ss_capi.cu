@@ -201,13 +201,14 @@ int ss_env_step(void* world, const SsBuffers* buf, const SsStepIO* io, void* str
 
 int ss_world_step(void* world, const SsBuffers* buf, const float* const* forces,
                   const uint64_t* decode_mask, int32_t count, const int32_t* guard,
-                  int32_t* d_status, void* stream) {
+                  int32_t guard_count, int32_t* d_status, void* stream) {
   World* w = static_cast<World*>(world);
   if (!w || !buf) { set_error("null argument"); return SS_ERR_CONTRACT; }
   SsStepIO io;
   memset(&io, 0, sizeof(io));
   io.actions = forces;
   io.guard = guard;
+  io.guard_count = guard_count;
   io.mode = SS_DO_PHYSICS | (count ? SS_DO_COUNT : 0);
   return launch_generic(*w, buf, &io, decode_mask, d_status, static_cast<cudaStream_t>(stream));
 }

@@ -22,6 +22,7 @@ struct GenericArgs {
   uint64_t decode_mask[kGenericMaxAgents / 64];  // bit i: decode_action applies
   int mode;
   const int* guard;
+  int guard_n;          // guard words to OR (SsStepIO.guard_count, >= 1)
   int* status;   // set to 1 when an unsupported shape pair is met
 };
 
@@ -61,7 +62,7 @@ SS_DEV bool joint_force(V2 pa, V2 pb, float target, float stiff, float k, float&
 __global__ void __launch_bounds__(32) k_generic_physics(const GenericArgs a) {
   extern __shared__ float sm[];
   grid_dep_sync();
-  if (a.guard && *a.guard) return;
+  if (guard_tripped(a.guard, a.guard_n)) return;
   const int lane = threadIdx.x;
   const int64_t B = a.s.B;
   const int64_t e = (int64_t)blockIdx.x * 32 + lane;
@@ -187,6 +188,7 @@ int launch_generic(World& w, const SsBuffers* buf, const SsStepIO* io, const uin
   }
   a.mode = io->mode;
   a.guard = io->guard;
+  a.guard_n = io->guard_count > 0 ? io->guard_count : 1;
   a.status = d_status;
   if (!(io->mode & (SS_DO_PHYSICS | SS_DO_COUNT))) return SS_OK;
   const size_t shmem = (size_t)3 * a.E * 32 * sizeof(float);

@@ -103,6 +103,16 @@ SS_DEV void grid_dep_sync() {
 
 bool pdl_enabled();   // SS_NO_PDL unset
 
+// The NaN verdict (SsStepIO.guard): the launch is a no-op when any of its n
+// guard words is set — word k is step k's action scan inside a multi-step
+// graph, so step k stops on a NaN in any action set up to its own.
+SS_DEV bool guard_tripped(const int* g, int n) {
+  if (g == nullptr) return false;
+  int any = 0;
+  for (int i = 0; i < n; ++i) any |= g[i];
+  return any != 0;
+}
+
 template <typename... KArgs, typename... Args>
 inline void launch_step(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                         Args... args) {

@@ -46,6 +46,7 @@ struct LargeArgs {
   int mode;
   int raw_forces;
   const int* guard;
+  int guard_n;          // guard words to OR (SsStepIO.guard_count, >= 1)
   int NA, NL, O;     // agents, landmarks (points / food), obs width
   int W;             // flag words
   float dmin;        // discovery: f32(r_a + r_b)
@@ -303,7 +304,7 @@ template <int T, int VEC>
 __global__ void __launch_bounds__(32 * kLargeWarps, SS_LARGE_MINB) k_discovery(const LargeArgs a) {
   extern __shared__ __align__(16) float smem[];
   grid_dep_sync();
-  if (a.guard && *a.guard) return;
+  if (guard_tripped(a.guard, a.guard_n)) return;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t B = a.s.B;
   const int64_t e = (int64_t)blockIdx.x * kLargeWarps + wid;
@@ -497,7 +498,7 @@ template <int T, int VEC>
 __global__ void __launch_bounds__(32 * kLargeWarps, SS_LARGE_MINB) k_dispersion(const LargeArgs a) {
   extern __shared__ __align__(16) float smem[];
   grid_dep_sync();
-  if (a.guard && *a.guard) return;
+  if (guard_tripped(a.guard, a.guard_n)) return;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t B = a.s.B;
   const int64_t e = (int64_t)blockIdx.x * kLargeWarps + wid;
@@ -679,6 +680,7 @@ int launch_large(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_
   a.mode = io->mode;
   a.raw_forces = io->raw_forces;
   a.guard = io->guard;
+  a.guard_n = io->guard_count > 0 ? io->guard_count : 1;
   a.dmin = w.d.sc[0];
   a.d2_act = w.d.sc[2];
   a.thr2 = w.d.sc[3];

@@ -41,6 +41,7 @@ struct SmallArgs {
   int obs_dim;
   int64_t e_begin;      // first env handled by this launch (tail launches)
   const int* guard;
+  int guard_n;          // guard words to OR (SsStepIO.guard_count, >= 1)
   float sc[16];
   double sd[8];
   int si[8];
@@ -211,7 +212,7 @@ template <int NA>
 __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_simple_spread(const SmallArgs a) {
   extern __shared__ __align__(16) float smem[];
   grid_dep_sync();
-  if (a.guard && *a.guard) return;
+  if (guard_tripped(a.guard, a.guard_n)) return;
   constexpr int O = SpreadEnv<NA>::O;
   const int64_t B = a.s.B;
   const int64_t e = a.e_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -293,7 +294,7 @@ __global__ void __launch_bounds__(kPipeTile) k_simple_spread_pipe(const SmallArg
   extern __shared__ __align__(16) float smem_pipe[];
   PipeSmem<NA>& S = *reinterpret_cast<PipeSmem<NA>*>(smem_pipe);
   grid_dep_sync();
-  if (a.guard && *a.guard) return;
+  if (guard_tripped(a.guard, a.guard_n)) return;
   constexpr int O = SpreadEnv<NA>::O;
   const int tid = threadIdx.x;
   const int64_t B = a.s.B;
@@ -388,7 +389,7 @@ template <int NA, int REV>
 __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_transport(const SmallArgs a) {
   extern __shared__ __align__(16) float smem[];
   grid_dep_sync();
-  if (a.guard && *a.guard) return;
+  if (guard_tripped(a.guard, a.guard_n)) return;
   constexpr int O = REV ? 10 : 12;
   const int64_t B = a.s.B;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -514,7 +515,7 @@ template <int NA>
 __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_dropout(const SmallArgs a) {
   extern __shared__ __align__(16) float smem[];
   grid_dep_sync();
-  if (a.guard && *a.guard) return;
+  if (guard_tripped(a.guard, a.guard_n)) return;
   constexpr int O = 4 + 2 * NA;
   const int64_t B = a.s.B;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -605,7 +606,7 @@ template <int NA>
 __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_wheel(const SmallArgs a) {
   extern __shared__ __align__(16) float smem[];
   grid_dep_sync();
-  if (a.guard && *a.guard) return;
+  if (guard_tripped(a.guard, a.guard_n)) return;
   constexpr int O = 10;
   const int64_t B = a.s.B;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -655,7 +656,7 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_wheel(const Sm
 __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_give_way(const SmallArgs a) {
   extern __shared__ __align__(16) float smem[];
   grid_dep_sync();
-  if (a.guard && *a.guard) return;
+  if (guard_tripped(a.guard, a.guard_n)) return;
   constexpr int O = 12;
   const int64_t B = a.s.B;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -714,7 +715,7 @@ template <int NA>
 __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_passage(const SmallArgs a) {
   extern __shared__ __align__(16) float smem[];
   grid_dep_sync();
-  if (a.guard && *a.guard) return;
+  if (guard_tripped(a.guard, a.guard_n)) return;
   constexpr int O = 10 + 2 * (NA - 1);
   const int64_t B = a.s.B;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -790,7 +791,7 @@ template <int NA>
 __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_balance(const SmallArgs a) {
   extern __shared__ __align__(16) float smem[];
   grid_dep_sync();
-  if (a.guard && *a.guard) return;
+  if (guard_tripped(a.guard, a.guard_n)) return;
   constexpr int O = 17;
   const int64_t B = a.s.B;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -851,7 +852,7 @@ template <int NA>
 __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_waterfall(const SmallArgs a) {
   extern __shared__ __align__(16) float smem[];
   grid_dep_sync();
-  if (a.guard && *a.guard) return;
+  if (guard_tripped(a.guard, a.guard_n)) return;
   const int NB = a.si[2];
   const int O = a.obs_dim;   // 6 + 2 NB
   const int64_t B = a.s.B;
@@ -947,7 +948,7 @@ template <int NA>
 __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_football(const SmallArgs a) {
   extern __shared__ __align__(16) float smem[];
   grid_dep_sync();
-  if (a.guard && *a.guard) return;
+  if (guard_tripped(a.guard, a.guard_n)) return;
   constexpr int NT = NA / 2;
   constexpr int O = 4 + 2 + 2 + 2 * (NA - 1) + 2;
   const int64_t B = a.s.B;
@@ -1252,7 +1253,7 @@ template <int NA>
 __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_flocking(const SmallArgs a, const FlockLidarK lk) {
   extern __shared__ __align__(16) float smem_raw[];
   grid_dep_sync();
-  if (a.guard && *a.guard) return;
+  if (guard_tripped(a.guard, a.guard_n)) return;
   const int NO = a.si[4];
   const int O = a.obs_dim;
   // shared memory: [per-ray best hits: n_rays x kSmallThreads doubles]
@@ -1448,7 +1449,7 @@ __global__ void __launch_bounds__(32 * NA, (SS_FLOCK_WARPS / NA < 32 ? SS_FLOCK_
     k_flocking_w(const SmallArgs a, const FlockLidarK lk) {
   extern __shared__ __align__(16) float smem_w[];
   grid_dep_sync();
-  if (a.guard && *a.guard) return;
+  if (guard_tripped(a.guard, a.guard_n)) return;
   const int NO = a.si[4];
   const int O = a.obs_dim;
   const int P = O | 1;
@@ -1691,6 +1692,7 @@ int launch_small(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_
   a.raw_forces = io->raw_forces;
   a.obs_dim = w.d.obs_dim;
   a.guard = io->guard;
+  a.guard_n = io->guard_count > 0 ? io->guard_count : 1;
   memcpy(a.sc, w.d.sc, sizeof(a.sc));
   memcpy(a.sd, w.d.sd, sizeof(a.sd));
   memcpy(a.si, w.d.si, sizeof(a.si));

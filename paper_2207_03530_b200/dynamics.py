@@ -93,13 +93,14 @@ def physics_world(world: World):
 
 
 def run_world_step(world: World, forces: list, decode_mask: int, count: bool, stream=None,
-                   guard=None) -> None:
+                   guard=None, guard_count: int = 1) -> None:
     """Launch the generic step kernel.
 
     forces[a]: agent a's (B, 2) f32 device tensor, or its data pointer (int).
     decode_mask bit a: apply decode_action's clip * u_multiplier on device.
-    guard: optional (1,) int32 device flag from ss_check_actions; a nonzero
-    flag (NaN action) turns the launch into a no-op (env.py:85: nothing moves).
+    guard: optional int32 device flags from ss_check_actions (guard_count
+    words); any nonzero word (a NaN action) turns the launch into a no-op
+    (env.py:85: nothing moves).
     """
     h = physics_world(world)
     ptrs = (ctypes.c_void_p * max(1, len(forces)))()
@@ -109,7 +110,7 @@ def run_world_step(world: World, forces: list, decode_mask: int, count: bool, st
     status = torch.zeros(1, dtype=torch.int32, device=world.device)
     st = stream if stream is not None else N.stream_handle(world.device)
     N.check(N.lib().ss_world_step(h.handle, world.buffers_ref(), ptrs, mask, int(count), N.ptr(guard),
-                                  N.ptr(status), st))
+                                  int(guard_count), N.ptr(status), st))
 
 
 def world_step(world: World, actions: list) -> None:

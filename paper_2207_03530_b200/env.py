@@ -360,22 +360,20 @@ class Env:
             infos = [sc.info(a, world) for a in self.agents]
         return StepResult(obs=obs_list, rewards=list(rew.unbind(0)), dones=done, infos=infos)
 
-    def _capture_step(self, ptrs, keepalive, flag=None) -> StepResult:
-        """One fused step without host syncs (graph capture).  flag: a device
-        int32 the step's NaN scan ORs into; a set flag makes the launch a
-        no-op (the guard of the eager validated step, left for the host to
-        read after the replay instead of syncing inside it)."""
+    def _capture_step(self, ptrs, keepalive, flags=None, n_flags: int = 1) -> StepResult:
+        """One fused step without host syncs (graph capture).  flags: device
+        int32 NaN verdicts of this and the earlier steps of the replay (their
+        action scans run on a side branch of the graph); any set word makes
+        the launch a no-op — the eager validated step's guard, left for the
+        host to read after the replay instead of syncing inside it."""
         saved = self.validate
         self.validate = False
         try:
-            if flag is None:
+            if flags is None:
                 return self._step_fused_ptrs(ptrs, keepalive, False)
             st = torch.cuda.current_stream(self.device).cuda_stream
-            h = self.scenario.native_handle(self.world)
-            arr = (N.c_vp * max(1, len(ptrs)))(*ptrs)
-            N.check(N.lib().ss_check_actions(h.handle, arr, flag.data_ptr(), st))
-            obs, rew, done = self.scenario.launch(self.world, N.MODE_STEP, action_ptrs=ptrs, guard=flag,
-                                                  flip_rng=False, stream=st)
+            obs, rew, done = self.scenario.launch(self.world, N.MODE_STEP, action_ptrs=ptrs, guard=flags,
+                                                  flip_rng=False, stream=st, guard_count=n_flags)
             B = self.batch_size
             obs_list = list((obs if obs.shape[1] == B else obs[:, :B]).unbind(0))
             return StepResult(obs=obs_list, rewards=list(rew.unbind(0)), dones=done,
@@ -456,7 +454,7 @@ class StepGraph:
         if validate and self._generic:
             raise ContractViolation("StepGraph(validate=True) covers the fused built-in step")
         # NaN verdict of the replay (validate=True), zeroed at its start
-        self.nan_flag = torch.zeros(1, dtype=torch.int32, device=env.device) if validate else None
+        self.nan_flag = torch.zeros(S, dtype=torch.int32, device=env.device) if validate else None
         sc, world = env.scenario, env.world
         self._rng_mode = bool(getattr(sc, "advances_rng_per_step", False))
         world.ensure_device_rng()
@@ -506,18 +504,44 @@ class StepGraph:
                 g = torch.cuda.CUDAGraph()
                 results = []
                 with torch.cuda.stream(stream), torch.cuda.graph(g, stream=stream):
-                    if self.nan_flag is not None:
-                        self.nan_flag.zero_()
+                    scanned = self._capture_scans(env, acts, i, A, B, S, stream) if self.nan_flag is not None else None
                     for k in range(S):
                         act = acts[(i + k) % len(acts)]
                         if self._generic:
                             results.append(self._capture_generic(act))
                             continue
                         base, stride = act.data_ptr(), B * 8
+                        if scanned is not None:
+                            stream.wait_event(scanned[k])
                         results.append(env._capture_step([base + a * stride for a in range(A)], act,
-                                                         self.nan_flag))
+                                                         self.nan_flag, k + 1))
+                    if scanned is not None:
+                        stream.wait_stream(self._side)
                 self._graphs[(cur, i)] = g
                 self._results[(cur, i)] = results
+
+    def _capture_scans(self, env, acts, i, A, B, S, stream) -> list:
+        """The replay's S action NaN scans (ss_check_actions) on a side branch
+        of the graph: they depend only on the action buffers, so they run
+        alongside the steps; step k waits for scan k (one event each)."""
+        if not hasattr(self, "_side"):
+            self._side = torch.cuda.Stream(env.device)
+        side = self._side
+        side.wait_stream(stream)           # fork from the capturing stream
+        h = env.scenario.native_handle(env.world)
+        events = []
+        with torch.cuda.stream(side):
+            self.nan_flag.zero_()
+            for k in range(S):
+                act = acts[(i + k) % len(acts)]
+                base, stride = act.data_ptr(), B * 8
+                arr = (N.c_vp * A)(*[base + a * stride for a in range(A)])
+                N.check(N.lib().ss_check_actions(h.handle, arr, self.nan_flag[k:].data_ptr(),
+                                                 side.cuda_stream))
+                ev = torch.cuda.Event()
+                ev.record(side)
+                events.append(ev)
+        return events
 
     def _capture_generic(self, act) -> StepResult:
         env = self.env

@@ -109,7 +109,8 @@ class FusedScenario(Scenario):
         return obs, rew, done
 
     def launch(self, world: World, mode: int, action_ptrs=None, raw_forces: bool = False,
-               guard=None, flip_rng: bool = True, stream: int | None = None, horizon: bool = True):
+               guard=None, flip_rng: bool = True, stream: int | None = None, horizon: bool = True,
+               guard_count: int = 1):
         """One fused launch in `mode`; returns (obs (A, Bp, O), rew (A, B), done (B,)).
 
         action_ptrs: one device pointer per agent to a contiguous (B, 2) f32
@@ -122,7 +123,7 @@ class FusedScenario(Scenario):
             from ..dynamics import run_world_step
 
             run_world_step(world, action_ptrs, decode_mask=0 if raw_forces else (1 << 256) - 1,
-                           count=False, stream=st, guard=guard)
+                           count=False, stream=st, guard=guard, guard_count=guard_count)
             mode &= ~N.DO_PHYSICS
         obs, rew, done = self.alloc_outputs(world, h.obs_dim)
         io = h.io
@@ -135,6 +136,7 @@ class FusedScenario(Scenario):
         io.done = done.data_ptr()
         io.mode = mode
         io.guard = guard.data_ptr() if guard is not None else None
+        io.guard_count = int(guard_count)
         io.raw_forces = int(raw_forces)
         N.check(N.lib().ss_env_step(h.handle, world.buffers_ref(), h.io_ref, st))
         if flip_rng and (mode & N.DO_POST) and self.advances_rng_per_step:

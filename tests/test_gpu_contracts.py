@@ -105,3 +105,31 @@ def test_reset_at_selectors(cuda):
     np.testing.assert_array_equal(state(e), state(ref))
     with pytest.raises(S.ContractViolation, match="ambiguous"):
         e.reset_at(np.array([0, 1, 0, 0, 1, 0]))
+
+
+def test_validated_step_graph(cuda):
+    """StepGraph(validate=True): the NaN scans run on a side branch of the
+    graph; clean replays equal eager validated stepping, and a NaN in step k
+    of a replay stops steps k.. (nothing moves from there), like the eager
+    step that raises at k."""
+    B, S_ = 200, 4
+    ref = S.Env(S.create_scenario("transport"), B, seed=6, device=cuda)
+    e = S.Env(S.create_scenario("transport"), B, seed=6, device=cuda, validate=False)
+    plans = G.pregen_actions(4, B, 2 * S_, 9)
+    bufs = [torch.from_numpy(np.stack(p)).to(cuda) for p in plans]
+    graph = e.step_graph(bufs, steps_per_replay=S_, validate=True)
+    outs = graph.rollout(0)
+    graph.check()
+    for k in range(S_):
+        r = ref.step(plans[k])
+        for x, y in zip(r.obs + r.rewards, outs[k].obs + outs[k].rewards):
+            assert torch.equal(x, y)
+    np.testing.assert_array_equal(state(e), state(ref))
+    # NaN in the third step of the next replay
+    bufs[S_ + 2][1, 17, 0] = float("nan")
+    for k in range(S_, S_ + 2):
+        ref.step(plans[k])
+    graph.rollout(S_)
+    with pytest.raises(S.ContractViolation, match="NaN"):
+        graph.check()
+    np.testing.assert_array_equal(state(e), state(ref))

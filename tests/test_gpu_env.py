@@ -167,37 +167,98 @@ def test_live_oracle_parity_with_masked_resets(cuda, name, ov, B, steps, seed):
                 np.testing.assert_array_equal(x.cpu().numpy(), y)
 
 
+class _GlobalDraws:
+    """The full batch's random stream as a sample of its envs sees it: every
+    uniform(lo, hi, n) of the sampled oracle consumes the whole batch's block
+    of Bg draws (numpy Philox, batching.py:185-186) and returns the sampled
+    envs' values — discovery's per-step relocation draws (discovery.py:66-68)
+    at their global indices."""
+
+    def __init__(self, state, Bg, idx):
+        self.g = np.random.Generator(np.random.Philox())
+        self.g.bit_generator.state = state
+        self.Bg, self.idx = Bg, np.asarray(idx)
+
+    def uniform(self, lo, hi, n):
+        raw = self.g.bit_generator.random_raw(self.Bg)[self.idx]
+        d = (raw >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+        return np.float64(lo) + (np.float64(hi) - np.float64(lo)) * d
+
+
+def _rng_words(st):
+    return ([int(x) for x in st["state"]["counter"]], [int(x) for x in st["state"]["key"]],
+            int(st["buffer_pos"]))
+
+
 @pytest.mark.parametrize("name,B", [("simple_spread", 1_000_000), ("transport", 100_000),
-                                    ("flocking", 100_000), ("discovery", 262_144), ("dispersion", 65_536)])
+                                    ("flocking", 100_000), ("discovery", 262_144), ("dispersion", 262_144)])
 def test_full_size_sampled_envs_match_oracle(cuda, name, B):
     """BASELINE sizes: the whole-batch reset is checked for every env against
-    numpy's Philox; 3 steps are checked on a sample of 256 envs (envs are
-    independent, so the oracle runs on the sample alone)."""
+    numpy's Philox; 4 steps are checked on a sample of 256 envs (envs are
+    independent, so the oracle runs on the sample alone; discovery's
+    relocations are drawn at the sampled envs' global stream positions and
+    the device's Philox state is checked after every step)."""
     from bench import WORKLOADS
 
-    scen, ov, _ = WORKLOADS[name]
+    scen, ov = WORKLOADS[name][:2]
     e = env(scen, B=B, cuda=cuda, seed=0, validate=False, ov=ov)
-    o = O.OracleEnv(scen, B, seed=0, **ov)
+    o = O.OracleEnv(scen, B, seed=0, reset=False, **ov)
+    o._apply_ops(None)                  # the whole-batch reset, without B x O observations
+    o.task.reset_aux(B, None)
     np.testing.assert_array_equal(state(e), ostate(o))
     idx = np.sort(np.random.default_rng(1).choice(B, 256, replace=False))
-    sub = O.OracleEnv(scen, 256, seed=0, reset=False, **ov)
+    idx[0], idx[-1] = 0, B - 1          # both ends of the batch
+    idx = np.unique(idx)
+    n = len(idx)
+    sub = O.OracleEnv(scen, n, seed=0, reset=False, **ov)
     sub.ws = o.ws.take(idx)
-    if hasattr(sub.task, "reset_aux"):
-        sub.task.reset_aux(256, None)
+    sub.task.reset_aux(n, None)
+    sub.rng = _GlobalDraws(o.rng.bit_generator.state, B, idx)
+    idx_t = torch.from_numpy(idx).to(cuda)
     A = len(e.agents)
     g = torch.Generator(device=cuda)
     g.manual_seed(5)
-    for t in range(3):
+    for t in range(4):
         acts = torch.rand((A, B, 2), device=cuda, generator=g) * 2.4 - 1.2
         r = e.step(acts)
-        a_np = acts.cpu().numpy()[:, idx]
-        obs, rew, done = sub.step(list(a_np))
-        if scen == "discovery":
-            break       # relocation draws depend on global indices: checked by the golden/live tests
-        np.testing.assert_array_equal(state(e)[:, :, idx], ostate(sub))
+        obs, rew, done = sub.step(list(acts[:, idx_t].cpu().numpy()))
+        np.testing.assert_array_equal(state(e)[:, :, idx], ostate(sub), err_msg=f"state @ {t}")
         for x, y in zip(r.obs, obs):
-            np.testing.assert_array_equal(x.cpu().numpy()[idx], y)
-        np.testing.assert_array_equal(torch.stack(r.rewards).cpu().numpy()[:, idx], np.stack(rew))
+            np.testing.assert_array_equal(x[idx_t].cpu().numpy(), y)
+        np.testing.assert_array_equal(torch.stack(r.rewards)[:, idx_t].cpu().numpy(), np.stack(rew))
+        np.testing.assert_array_equal(r.dones[idx_t].cpu().numpy(), done)
+        if scen == "discovery":
+            assert _rng_words(e.rng.state()) == _rng_words(sub.rng.g.bit_generator.state), f"rng @ {t}"
+            assert int(e.world.flags[0, idx_t].ne(0).sum()) == int(sub.task.covered.any(1).sum())
+        del r
+
+
+def test_discovery64_two_shards_equal_unsharded_at_size(cuda):
+    """BASELINE config 5 (discovery, 64 agents, 262144 envs): two shards (one
+    Env each, their global offsets) equal the unsharded run bitwise — state,
+    observations, rewards, relocation draws."""
+    Bg, ov = 262_144, {"n_agents": 64}
+    full = env("discovery", B=Bg, cuda=cuda, seed=2, validate=False, ov=ov)
+    shards = []
+    for r in range(2):
+        off, cnt = shard_range(r, 2, Bg)
+        shards.append((off, cnt, S.Env(S.create_scenario("discovery", **ov), cnt, seed=2, device=cuda,
+                                       validate=False, env_offset=off, global_batch=Bg)))
+    g = torch.Generator(device=cuda)
+    g.manual_seed(3)
+    for t in range(3):
+        acts = torch.rand((64, Bg, 2), device=cuda, generator=g) * 2 - 1
+        rf = full.step(acts)
+        for off, cnt, e in shards:
+            rs = e.step(acts[:, off:off + cnt].contiguous())
+            for x, y in zip(rf.obs[::9], rs.obs[::9]):
+                assert torch.equal(x[off:off + cnt], y), f"obs @ {t}"
+            assert torch.equal(torch.stack(rf.rewards)[:, off:off + cnt], torch.stack(rs.rewards))
+            assert _rng_words(e.rng.state()) == _rng_words(full.rng.state())
+            del rs
+        del rf
+    for off, cnt, e in shards:
+        assert torch.equal(e.world.state_array(), full.world.state_array()[:, :, off:off + cnt])
 
 
 VARIANTS = [

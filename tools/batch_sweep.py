@@ -54,7 +54,7 @@ def main() -> None:
         print(json.dumps({"probe": "1-element kernel graph", "kernel_ms": float(np.median([a.elapsed_time(b) for a, b in ev])),
                           "ms_per_step": ev[0][0].elapsed_time(ev[-1][1]) / len(ev)}))
         return
-    scen, ov, _ = WORKLOADS[args.scenario]
+    scen, ov, _ = WORKLOADS[args.scenario][:3]
     hbm = peaks()["hbm_gbs"]
     for B in args.sizes:
         env = Env(create_scenario(scen, **ov), B, seed=0, device=dev, validate=False)

@@ -2,8 +2,9 @@
 # Profiling runs for profiles/ (execute on the GPU box via gpurun, 1 GPU; one
 # ncu invocation per gpurun call):
 #   bash tools/profile_all.sh launches     bench plainly, then its ncu launch list
-#   bash tools/profile_all.sh SCENARIO     step loop plainly, then one ncu --set full
+#   [ENVS=n] bash tools/profile_all.sh SCENARIO   step loop plainly, then one ncu --set full
 #                                          capture of the fused kernel in steady state
+#                                          (ENVS: batch size, default the workload's)
 # Summaries land in gpurun_out/ (tools/ncu_summary.py); the .ncu-rep is deleted
 # to keep the merge-back small.
 set -u
@@ -24,10 +25,13 @@ declare -A KERN=([simple_spread]=k_simple_spread [transport]=k_transport [flocki
 # gather at the beacon after ~1k steps; the others settle within tens)
 declare -A PRE=([simple_spread]=20 [transport]=200 [flocking]=1500 [dispersion]=20 [discovery]=50)
 s=$what
-CMD="python tools/step_loop.py $s 0 $((${PRE[$s]} + 2))"
-$CMD > $OUT/plain_$s.log 2>&1 && \
+ENVS=${ENVS:-0}
+tag=$s${ENVS/#0/}
+[ "$ENVS" != 0 ] && tag=${s}_$ENVS
+CMD="python tools/step_loop.py $s $ENVS $((${PRE[$s]} + 2))"
+$CMD > $OUT/plain_$tag.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:${KERN[$s]} -s ${PRE[$s]} -c 1 \
-      -o $OUT/full_$s $CMD > $OUT/ncu_full_$s.log 2>&1
-echo "$s: $?"
-[ -f $OUT/full_$s.ncu-rep ] && python tools/ncu_summary.py $OUT/full_$s.ncu-rep $OUT/full_$s && rm -f $OUT/full_$s.ncu-rep
+      -o $OUT/full_$tag $CMD > $OUT/ncu_full_$tag.log 2>&1
+echo "$tag: $?"
+[ -f $OUT/full_$tag.ncu-rep ] && python tools/ncu_summary.py $OUT/full_$tag.ncu-rep $OUT/full_$tag && rm -f $OUT/full_$tag.ncu-rep
 exit 0

@@ -17,7 +17,7 @@ from paper_2207_03530_b200 import Env, create_scenario  # noqa: E402
 
 def main() -> None:
     name = sys.argv[1] if len(sys.argv) > 1 else "simple_spread"
-    scen, ov, default_b = WORKLOADS[name]
+    scen, ov, default_b = WORKLOADS[name][:3]
     B = int(sys.argv[2]) if len(sys.argv) > 2 and int(sys.argv[2]) > 0 else default_b
     steps = int(sys.argv[3]) if len(sys.argv) > 3 else 4
     env = Env(create_scenario(scen, **ov), B, seed=0, device="cuda:0", validate=False)

@@ -22,7 +22,7 @@ from bench import WORKLOADS, bytes_per_env_step, peaks
 from paper_2207_03530_b200 import Env, create_scenario
 out = {}
 for name in %(names)r:
-    scen, ov, B = WORKLOADS[name]
+    scen, ov, B = WORKLOADS[name][:3]
     env = Env(create_scenario(scen, **ov), B, seed=0, device="cuda:0", validate=False)
     A = len(env.agents); O = env.observations()[0].shape[1]
     acts = [torch.rand((A, B, 2), device="cuda:0") * 2 - 1 for _ in range(2)]
