@@ -100,12 +100,37 @@ typedef struct SsPairDesc {
                              active iff x*x+y*y <= d2_act (no sqrt needed)     */
 } SsPairDesc;
 
-/* One reset action in scenario call order (common.py:11-34). */
+/* The reset program: one instruction per reference reset action, in the
+ * scenario's call order (reset_world_at: common.py:11-34 scatter / place,
+ * plus the catalog tasks' relative placements and angle draws).  Per env it
+ * runs on a float32 register file R[SS_RESET_REGS]: the reference's draws
+ * are float32 (SeededRng.uniform casts, batching.py:185-186) and Python-float
+ * operands meeting them stay float32 (NEP 50), so every value a reset program
+ * combines is a float32.  Every draw instruction takes the next draw slot
+ * (x before y), so a whole-batch reset reads draw slot*Bg + e and the env of
+ * rank r in a masked reset reads r*n_slots + slot (= sequential
+ * reset(env_index=i) calls in ascending i). */
+typedef enum SsResetKind {
+  SS_RESET_SCATTER = 0,   /* pos = f32(lo + range * u) per axis (2 slots); zero motion      */
+  SS_RESET_PLACE = 1,     /* pos = (f32(lo_x), f32(lo_y)); zero motion                      */
+  SS_RESET_DRAW = 2,      /* R[r0] = f32(lo_x + range_x * u)               (1 slot)         */
+  SS_RESET_CONST = 3,     /* R[r0] = f32(lo_x)                                              */
+  SS_RESET_ADD = 4,       /* R[r0] = R[r1] + R[r2]   (float32)                              */
+  SS_RESET_NEG = 5,       /* R[r0] = -R[r1]                                                 */
+  SS_RESET_LOADPOS = 6,   /* R[r0] = pos[entity][axis]                                      */
+  SS_RESET_SETPOS = 7,    /* pos[entity] = (R[r0], R[r1]); velocity kept                     */
+  SS_RESET_SETROT = 8,    /* rot[entity] = R[r0]                                            */
+  SS_RESET_ZERO = 9       /* zero_motion: vel = 0, ang_vel = 0 (core.py:94-103)              */
+} SsResetKind;
+#define SS_RESET_REGS 16
+
 typedef struct SsResetOp {
-  int32_t entity;         /* entity index */
-  int32_t kind;           /* 0 = scatter (2 draws), 1 = place */
-  double lo_x, lo_y;      /* scatter: lower corner | place: x, y */
-  double range_x, range_y;/* scatter: hi - lo (float64, as numpy computes)    */
+  int32_t entity;         /* entity index (-1 for register-only instructions) */
+  int32_t kind;           /* SsResetKind */
+  double lo_x, lo_y;      /* scatter: lower corner | place: x, y | draw: low | const: value */
+  double range_x, range_y;/* scatter / draw: hi - lo (float64, as numpy computes) */
+  int32_t r0, r1, r2;     /* register operands */
+  int32_t axis;           /* loadpos: 0 = x, 1 = y */
 } SsResetOp;
 
 /* Distance joint (extension; the reference has none — SPEC.md:204 lists

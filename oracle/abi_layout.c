@@ -14,7 +14,7 @@ int main(void) {
   Z(SsEntityDesc); F(SsEntityDesc, shape); F(SsEntityDesc, slot); F(SsEntityDesc, dim0);
   F(SsEntityDesc, dim1); F(SsEntityDesc, inv_m_dt); F(SsEntityDesc, u_mult);
   Z(SsPairDesc); F(SsPairDesc, d_min); F(SsPairDesc, sign); F(SsPairDesc, d2_act);
-  Z(SsResetOp); F(SsResetOp, lo_x); F(SsResetOp, range_y);
+  Z(SsResetOp); F(SsResetOp, lo_x); F(SsResetOp, range_y); F(SsResetOp, r0); F(SsResetOp, axis);
   Z(SsWorldDesc); F(SsWorldDesc, batch); F(SsWorldDesc, max_steps); F(SsWorldDesc, dt);
   F(SsWorldDesc, entities); F(SsWorldDesc, pairs); F(SsWorldDesc, reset_ops); F(SsWorldDesc, sc);
   F(SsWorldDesc, sd); F(SsWorldDesc, si); F(SsWorldDesc, lidar_rays); F(SsWorldDesc, lidar_max_range);

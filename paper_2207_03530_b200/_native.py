@@ -42,9 +42,15 @@ class SsPairDesc(ctypes.Structure):
     _fields_ = [("i", c_i32), ("j", c_i32), ("d_min", c_f32), ("sign", c_f32), ("d2_act", c_f32)]
 
 
+(RESET_SCATTER, RESET_PLACE, RESET_DRAW, RESET_CONST, RESET_ADD, RESET_NEG, RESET_LOADPOS, RESET_SETPOS,
+ RESET_SETROT, RESET_ZERO) = range(10)
+RESET_REGS = 16
+
+
 class SsResetOp(ctypes.Structure):
     _fields_ = [("entity", c_i32), ("kind", c_i32), ("lo_x", c_f64), ("lo_y", c_f64),
-                ("range_x", c_f64), ("range_y", c_f64)]
+                ("range_x", c_f64), ("range_y", c_f64), ("r0", c_i32), ("r1", c_i32), ("r2", c_i32),
+                ("axis", c_i32)]
 
 
 class SsJointDesc(ctypes.Structure):

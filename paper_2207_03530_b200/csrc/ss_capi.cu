@@ -110,8 +110,12 @@ static int validate_desc(const SsWorldDesc* d) {
   }
   for (int j = 0; j < d->n_reset_ops; ++j) {
     const SsResetOp& o = d->reset_ops[j];
-    if (o.entity < 0 || o.entity >= d->n_entities || (o.kind != 0 && o.kind != 1)) {
-      set_error("bad reset op"); return SS_ERR_CONTRACT;
+    const bool uses_entity = o.kind <= SS_RESET_PLACE || o.kind >= SS_RESET_LOADPOS;
+    const bool reg_ok = o.r0 >= 0 && o.r0 < SS_RESET_REGS && o.r1 >= 0 && o.r1 < SS_RESET_REGS &&
+                        o.r2 >= 0 && o.r2 < SS_RESET_REGS;
+    if (o.kind < SS_RESET_SCATTER || o.kind > SS_RESET_ZERO || !reg_ok || (o.axis != 0 && o.axis != 1) ||
+        (uses_entity && (o.entity < 0 || o.entity >= d->n_entities))) {
+      set_error("bad reset op " + std::to_string(j)); return SS_ERR_CONTRACT;
     }
   }
   return SS_OK;
@@ -139,8 +143,8 @@ int ss_world_create(const SsWorldDesc* desc, void** out_world) {
   w->pairs.assign(desc->pairs, desc->pairs + desc->n_pairs);
   w->reset_ops.assign(desc->reset_ops, desc->reset_ops + desc->n_reset_ops);
   if (desc->n_joints > 0) w->joints.assign(desc->joints, desc->joints + desc->n_joints);
-  w->n_scatter = 0;
-  for (const auto& o : w->reset_ops) w->n_scatter += (o.kind == 0);
+  w->n_slots = 0;     // draw slots per env: 2 per scatter, 1 per draw
+  for (const auto& o : w->reset_ops) w->n_slots += (o.kind == SS_RESET_SCATTER) ? 2 : (o.kind == SS_RESET_DRAW);
   if ((rc = upload(w->ents, &w->d_ents)) || (rc = upload(w->pairs, &w->d_pairs)) ||
       (rc = upload(w->reset_ops, &w->d_reset_ops)) || (rc = upload(w->joints, &w->d_joints))) {
     free_world(w);

@@ -254,17 +254,34 @@ int launch_np_trig(const float* x, float* out, int64_t n, int want_cos, cudaStre
 
 struct CheckArgs {
   const float* act[kGenericMaxAgents];
+  int A;
   int64_t n;   // floats per agent
+  int vec4;    // every agent block 16-byte aligned and n % 4 == 0
   int* flag;
 };
 
-__global__ void k_check_actions(const CheckArgs a) {
+// NaN scan of every agent's action block (env.py:85): one grid-stride pass
+// over all agents' floats (16-byte loads when aligned), the verdict ORed into
+// *flag.  Sized to the SM count, not to the agent count.
+__global__ void __launch_bounds__(512) k_check_actions(const CheckArgs a) {
   grid_dep_sync();
-  const float* p = a.act[blockIdx.y];
   bool bad = false;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    bad |= isnan(p[i]);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a.vec4) {
+    const int64_t n4 = a.n >> 2;
+    for (int i = 0; i < a.A; ++i) {
+      const float4* p = reinterpret_cast<const float4*>(a.act[i]);
+      for (int64_t k = t0; k < n4; k += stride) {
+        const float4 v = __ldcs(p + k);
+        bad |= isnan(v.x) | isnan(v.y) | isnan(v.z) | isnan(v.w);
+      }
+    }
+  } else {
+    for (int i = 0; i < a.A; ++i) {
+      const float* p = a.act[i];
+      for (int64_t k = t0; k < a.n; k += stride) bad |= isnan(p[k]);
+    }
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(a.flag, 1);
 }
@@ -275,12 +292,25 @@ int launch_check_actions(int n_agents, int64_t B, const float* const* actions, i
   if (n_agents == 0) return SS_OK;
   CheckArgs a;
   memset(&a, 0, sizeof(a));
-  for (int i = 0; i < n_agents; ++i) a.act[i] = actions[i];
+  a.vec4 = ((2 * B) % 4) == 0;
+  for (int i = 0; i < n_agents; ++i) {
+    a.act[i] = actions[i];
+    a.vec4 &= (reinterpret_cast<uintptr_t>(actions[i]) & 15u) == 0;
+  }
+  a.A = n_agents;
   a.n = 2 * B;
   a.flag = flag;
-  const int64_t want = (a.n + 255) / 256;
-  const unsigned gx = (unsigned)(want < 1184 ? want : 1184);
-  launch_step(k_check_actions, dim3(gx, n_agents), dim3(256), 0, st, a);
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const int64_t per_block = 512LL * (a.vec4 ? 4 : 1);
+  const int64_t want = (a.n + per_block - 1) / per_block;
+  const unsigned grid = (unsigned)(want < 4LL * sms ? (want > 0 ? want : 1) : 4LL * sms);
+  launch_step(k_check_actions, dim3(grid), dim3(512), 0, st, a);
   return cuda_status(cudaGetLastError(), "action check launch");
 }
 

@@ -26,7 +26,7 @@ struct World {
   double* d_lidar_dirs = nullptr;      // [lidar_rays][2]
   int64_t* d_scan = nullptr;           // masked-reset block scan scratch
   int64_t scan_cap = 0;
-  int n_scatter = 0;                   // scatter ops in the reset program
+  int n_slots = 0;                     // draw slots per env of the reset program
 };
 
 void set_error(const std::string& msg);

@@ -346,10 +346,13 @@ SS_HD void philox_advance(const uint64_t* st, uint64_t n, uint64_t* out) {
   out[10] = m - 4 * (blocks - 1);
 }
 
-// numpy random_uniform: off + scale * next_double, then .astype(float32).
-SS_HD float uniform_f32(uint64_t u, double lo, double range) {
+// numpy random_uniform: off + scale * next_double (float64).
+SS_HD double uniform_f64(uint64_t u, double lo, double range) {
   const double d = (double)(u >> 11) * (1.0 / 9007199254740992.0);
-  return (float)dadd_rn(lo, dmul_rn(range, d));
+  return dadd_rn(lo, dmul_rn(range, d));
 }
+
+// ... then .astype(float32).
+SS_HD float uniform_f32(uint64_t u, double lo, double range) { return (float)uniform_f64(u, lo, range); }
 
 }  // namespace ssm

@@ -576,7 +576,7 @@ class StepGraph:
     def check(self) -> None:
         """validate=True: raise ContractViolation if the last replay met a NaN
         action (the steps from that one on did not move anything).  Syncs."""
-        if self.nan_flag is not None and int(self.nan_flag.item()) != 0:
+        if self.nan_flag is not None and bool(self.nan_flag.any()):
             raise ContractViolation("an action replayed by this StepGraph contains NaN")
 
     def rollout(self, i: int = 0) -> list:

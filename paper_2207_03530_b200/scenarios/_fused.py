@@ -52,28 +52,26 @@ class FusedScenario(Scenario):
         return True
 
     # ---- descriptor ---------------------------------------------------------
+    def reset_program(self, world: World) -> "ResetProgram":
+        """The device reset program (SsResetOp); by default the scatter /
+        place list of reset_ops()."""
+        prog = ResetProgram()
+        for k, kind, lo, hi in self.reset_ops(world):
+            if kind == "scatter":
+                prog.scatter(k, lo, hi)
+            else:
+                prog.place(k, lo[0], lo[1])
+        return prog
+
     def native_desc(self, world: World, max_steps: int | None = None) -> "N.SsWorldDesc":
         if max_steps is None:
             max_steps = getattr(world, "max_steps", self.max_steps)
         d = world.base_desc(self.native_id, max_steps)
         d.obs_dim = self.obs_dim(world)
         d.n_flag_words = world.flags.shape[0]
-        ops = self.reset_ops(world)
-        arr = (N.SsResetOp * max(1, len(ops)))()
-        for n, (k, kind, lo, hi) in enumerate(ops):
-            arr[n].entity = k
-            if kind == "scatter":
-                lo64 = np.asarray(lo, dtype=np.float64)
-                hi64 = np.asarray(hi, dtype=np.float64)
-                arr[n].kind = 0
-                arr[n].lo_x, arr[n].lo_y = float(lo64[0]), float(lo64[1])
-                arr[n].range_x = float(hi64[0] - lo64[0])
-                arr[n].range_y = float(hi64[1] - lo64[1])
-            else:
-                arr[n].kind = 1
-                arr[n].lo_x, arr[n].lo_y = float(lo[0]), float(lo[1])
+        arr = self.reset_program(world).to_c()
         d.reset_ops = ctypes.cast(arr, ctypes.POINTER(N.SsResetOp))
-        d.n_reset_ops = len(ops)
+        d.n_reset_ops = arr._n
         self.fill_constants(world, d)
         d._keep = (d._keep, arr)
         return d
@@ -185,10 +183,103 @@ class FusedScenario(Scenario):
         world.rng.flip()
 
 
+class ResetProgram:
+    """Builder of a device reset program (include/swarmsim_b200.h SsResetOp):
+    the reference's reset_world_at restated as register instructions in its
+    call order.  Registers are float32, as every value the reference's resets
+    combine is (SeededRng.uniform returns float32, batching.py:185-186; Python
+    floats are weak, NEP 50); every draw() takes the next draw slot, exactly
+    one uniform() call of the reference (n = B for a whole reset, 1 for
+    reset(env_index))."""
+
+    def __init__(self):
+        self.ops: list[tuple] = []
+        self.n_regs = 0
+
+    def release(self) -> None:
+        """Every register value so far is dead: reuse the register file."""
+        self.n_regs = 0
+
+    def _reg(self) -> int:
+        if self.n_regs >= N.RESET_REGS:
+            raise ValueError("reset program needs more than 16 registers")
+        self.n_regs += 1
+        return self.n_regs - 1
+
+    def _op(self, kind, entity=-1, lo=(0.0, 0.0), rng=(0.0, 0.0), r=(0, 0, 0), axis=0):
+        self.ops.append((entity, kind, float(lo[0]), float(lo[1]), float(rng[0]), float(rng[1]), *r, axis))
+
+    # common.scatter / place (common.py:11-34)
+    def scatter(self, k: int, lo, hi) -> None:
+        lo64, hi64 = np.asarray(lo, dtype=np.float64), np.asarray(hi, dtype=np.float64)
+        self._op(N.RESET_SCATTER, k, lo64, hi64 - lo64)
+
+    def place(self, k: int, x: float, y: float) -> None:
+        self._op(N.RESET_PLACE, k, (x, y))
+
+    # register instructions
+    def draw(self, lo: float, hi: float) -> int:
+        """rng.uniform(lo, hi, (n,)): float32(lo + (hi - lo) * u)."""
+        r = self._reg()
+        self._op(N.RESET_DRAW, lo=(lo, 0.0), rng=(float(np.float64(hi) - np.float64(lo)), 0.0), r=(r, 0, 0))
+        return r
+
+    def const(self, c: float) -> int:
+        r = self._reg()
+        self._op(N.RESET_CONST, lo=(c, 0.0), r=(r, 0, 0))
+        return r
+
+    def add(self, a: int, b: int) -> int:
+        r = self._reg()
+        self._op(N.RESET_ADD, r=(r, a, b))
+        return r
+
+    def neg(self, a: int) -> int:
+        r = self._reg()
+        self._op(N.RESET_NEG, r=(r, a, 0))
+        return r
+
+    def loadpos(self, k: int, axis: int) -> int:
+        r = self._reg()
+        self._op(N.RESET_LOADPOS, k, r=(r, 0, 0), axis=axis)
+        return r
+
+    def setpos(self, k: int, rx: int, ry: int) -> None:
+        """state.set_pos_xy(x, y)."""
+        self._op(N.RESET_SETPOS, k, r=(rx, ry, 0))
+
+    def setrot(self, k: int, r: int) -> None:
+        self._op(N.RESET_SETROT, k, r=(r, 0, 0))
+
+    def zero(self, k: int) -> None:
+        """state.zero_motion (core.py:94-103)."""
+        self._op(N.RESET_ZERO, k)
+
+    def to_c(self):
+        arr = (N.SsResetOp * max(1, len(self.ops)))()
+        for n, op in enumerate(self.ops):
+            q = arr[n]
+            (q.entity, q.kind, q.lo_x, q.lo_y, q.range_x, q.range_y, q.r0, q.r1, q.r2, q.axis) = op
+        arr._n = len(self.ops)
+        return arr
+
+
+class RefHeuristic:
+    """Mixin: the scripted controller of the torch restatement (`_reference`,
+    scenarios/catalog.py), the reference's heuristic_action."""
+
+    _reference: type = None
+
+    def heuristic_action(self, agent_index: int, obs):
+        return self._reference.heuristic_action(self, agent_index, obs)
+
+
 class HostReset:
     """Mixin for fused scenarios whose reset program runs on the host: the
-    reference's own reset code (`_reference.reset_world_at`, drawing from the
-    Env's Philox stream), one env at a time, ascending, for masked resets."""
+    torch restatement's reset code (`_reference.reset_world_at`, drawing from
+    the Env's Philox stream), one env at a time, ascending, for masked
+    resets.  (Every built-in task now resets on the device; kept for user
+    subclasses with host reset programs.)"""
 
     _reference: type = None
     shardable_reset = False

@@ -5,20 +5,22 @@ reds' chase script runs on the device before the step (Env's host-decode
 path), physics (ball, fences and nets as line segments) is world_step's
 generic kernel, and the rest of the step — count, goal test, reward
 10 * right - 10 * left - 0.1 * gap for blues (0 for scripted reds), done,
-observation — is k_football<n> (csrc/ss_small.cu).  Resets run the
-reference's host program.
+observation — is k_football<n> (csrc/ss_small.cu).  Resets are a device
+reset program (ResetProgram).
 """
 from __future__ import annotations
+
+import numpy as np
 
 from .. import _native as N
 from ..core import World
 from . import register
-from ._fused import FusedScenario, HostReset, f32
+from ._fused import FusedScenario, RefHeuristic, ResetProgram, f32
 from .catalog import FIELD_HX, Football as _Reference
 
 
 @register("football")
-class Football(HostReset, FusedScenario):
+class Football(RefHeuristic, FusedScenario):
     native_id = N.SCN_FOOTBALL
     max_steps = 400
     _reference = _Reference
@@ -43,3 +45,31 @@ class Football(HostReset, FusedScenario):
         d.sc[1] = f32(0.1)
         d.sc[2] = f32(FIELD_HX)            # Vec2.full(B, FIELD_HX, 0.0): float32
         d.sd[0] = float(FIELD_HX)
+
+    def reset_program(self, world):
+        """football.py:100-138: blues and reds drawn (x then y) in their
+        halves, the ball jittered around the centre spot, fences and nets
+        placed (the side fences and the net backs upright)."""
+        from .catalog import FIELD_HY, MOUTH_HY, NET_DEPTH
+
+        p, idx = ResetProgram(), world.index_of
+        for i in range(self.n_per_team):
+            p.scatter(idx(world.entity(f"blue_{i}")), (-1.2, -0.7), (-0.3, 0.7))
+            p.scatter(idx(world.entity(f"red_{i}")), (0.3, -0.7), (1.2, 0.7))
+        p.scatter(idx(world.entity("ball")), (-0.1, -0.1), (0.1, 0.1))
+        mid = (MOUTH_HY + FIELD_HY) / 2
+        p.place(idx(world.entity("fence_top")), 0.0, FIELD_HY)
+        p.place(idx(world.entity("fence_bottom")), 0.0, -FIELD_HY)
+        up = p.const(np.pi / 2)
+        for side, sx in (("left", -FIELD_HX), ("right", FIELD_HX)):
+            for part, y in (("up", mid), ("down", -mid)):
+                f = idx(world.entity(f"fence_{side}_{part}"))
+                p.place(f, sx, y)
+                p.setrot(f, up)
+            bx = sx - NET_DEPTH if side == "left" else sx + NET_DEPTH
+            back = idx(world.entity(f"net_{side}_back"))
+            p.place(back, bx, 0.0)
+            p.setrot(back, up)
+            for edge, ey in (("up", MOUTH_HY), ("down", -MOUTH_HY)):
+                p.place(idx(world.entity(f"net_{side}_{edge}")), (sx + bx) / 2, ey)
+        return p

@@ -9,15 +9,17 @@ program.
 """
 from __future__ import annotations
 
+import numpy as np
+
 from .. import _native as N
 from ..core import World
 from . import register
-from ._fused import FusedScenario, HostReset, f32
+from ._fused import FusedScenario, RefHeuristic, ResetProgram, f32
 from .catalog import GiveWay as _Reference
 
 
 @register("give_way")
-class GiveWay(HostReset, FusedScenario):
+class GiveWay(RefHeuristic, FusedScenario):
     native_id = N.SCN_GIVE_WAY
     max_steps = 300
     _reference = _Reference
@@ -41,3 +43,22 @@ class GiveWay(HostReset, FusedScenario):
     def fill_constants(self, world, d):
         d.sc[0] = f32(0.15)
         d.sd[0], d.sd[1] = float(self.alcove[0]), float(self.alcove[1])
+
+    def reset_program(self, world):
+        """give_way.py:48-72: each agent drawn (x then y) at its corridor end,
+        goals, walls and the alcove (its side walls turned upright)."""
+        p, idx, hw = ResetProgram(), world.index_of, self.half_width
+        a0, a1 = world.agents
+        for agent, lo, hi in ((a0, -1.6, -1.4), (a1, 1.4, 1.6)):
+            p.scatter(idx(agent), (lo, -0.04), (hi, 0.04))     # x block, then y block
+        p.place(idx(world.entity("goal_0")), 1.5, 0.0)
+        p.place(idx(world.entity("goal_1")), -1.5, 0.0)
+        p.place(idx(world.entity("wall_bottom")), 0.0, -hw)
+        p.place(idx(world.entity("wall_top_left")), -1.15, hw)
+        p.place(idx(world.entity("wall_top_right")), 1.15, hw)
+        for name, x in (("alcove_left", -0.3), ("alcove_right", 0.3)):
+            k = idx(world.entity(name))
+            p.place(k, x, hw + 0.15)
+            p.setrot(k, p.const(np.pi / 2))
+        p.place(idx(world.entity("alcove_top")), 0.0, hw + 0.3)
+        return p

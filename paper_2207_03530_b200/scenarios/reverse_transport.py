@@ -6,21 +6,20 @@ agent-agent then (agent, crate) per agent; sphere-box contacts on the box
 perimeter), so the step is k_transport<n, 1> (csrc/ss_small.cu): the same
 physics and reward (-|crate - goal|, float32; done when < success_dist) with
 the reverse observation [x, y, vx, vy, crate - self, crate vel, goal - crate].
-Resets place the agents relative to the freshly drawn crate; they run the
-reference's host program (catalog.ReverseTransport.reset_world_at) on the
-Env's Philox stream, one env at a time for masked resets.
+Resets place the agents relative to the freshly drawn crate: a device
+reset program (float32 crate position plus float64 draws, ResetProgram).
 """
 from __future__ import annotations
 
 from ..core import World
 from . import register
-from ._fused import HostReset
+from ._fused import RefHeuristic
 from .catalog import ReverseTransport as _Reference
 from .transport import Transport
 
 
 @register("reverse_transport")
-class ReverseTransport(HostReset, Transport):
+class ReverseTransport(RefHeuristic, Transport):
     max_steps = 250
     _reference = _Reference
 
@@ -39,3 +38,25 @@ class ReverseTransport(HostReset, Transport):
     def fill_constants(self, world, d):
         super().fill_constants(world, d)
         d.si[1] = 1          # reverse observation layout
+
+    def reset_program(self, world):
+        """reverse_transport.py:53-67: the crate scattered and set level; each
+        agent at crate + uniform offset (float32 crate position plus a float64
+        draw, x then y), the goal scattered."""
+        from ._fused import ResetProgram
+
+        p, idx = ResetProgram(), world.index_of
+        crate = idx(world.entity("crate"))
+        p.scatter(crate, (-0.5, -0.5), (0.5, 0.5))
+        p.setrot(crate, p.const(0.0))
+        cx, cy = p.loadpos(crate, 0), p.loadpos(crate, 1)
+        inner = self.crate_size / 2 - 0.05 - 0.07
+        for agent in world.agents:
+            ax = p.draw(-inner, inner)
+            ay = p.draw(-inner, inner)
+            a = idx(agent)
+            p.setpos(a, p.add(cx, ax), p.add(cy, ay))
+            p.zero(a)
+            p.n_regs = 3          # register 0 (const) and cx, cy stay live
+        p.scatter(idx(world.entity("goal")), (-0.9, -0.9), (0.9, 0.9))
+        return p

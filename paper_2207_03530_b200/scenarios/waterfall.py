@@ -5,7 +5,7 @@ Physics (gravity, sphere-box contacts) is world_step's generic kernel,
 launched first; the rest of the step — count, reward -gap - penalty *
 (touching teammates + block bumps via closest points, float64), done when
 every agent is in the basin, observation — is k_waterfall<n>
-(csrc/ss_small.cu).  Resets run the reference's host program.
+(csrc/ss_small.cu).  Resets are a device reset program (ResetProgram).
 """
 from __future__ import annotations
 
@@ -13,12 +13,12 @@ from .. import _native as N
 from ..core import World
 from ..shapes import min_contact_distance
 from . import register
-from ._fused import FusedScenario, HostReset, f32
+from ._fused import FusedScenario, RefHeuristic, ResetProgram, f32
 from .catalog import BLOCKS, Waterfall as _Reference
 
 
 @register("waterfall")
-class Waterfall(HostReset, FusedScenario):
+class Waterfall(RefHeuristic, FusedScenario):
     native_id = N.SCN_WATERFALL
     max_steps = 200
     _reference = _Reference
@@ -45,3 +45,16 @@ class Waterfall(HostReset, FusedScenario):
         d.sc[2] = f32(0.2)
         d.sd[0] = float(self.collision_penalty)
         d.si[2] = len(BLOCKS)
+
+    def reset_program(self, world):
+        """waterfall.py:52-62: agents drawn (x then y) along the top; the basin
+        and the baffles placed."""
+        from .catalog import BASIN
+
+        p, idx = ResetProgram(), world.index_of
+        for agent in world.agents:
+            p.scatter(idx(agent), (-0.6, 0.75), (0.6, 0.95))
+        p.place(idx(world.entity("basin")), *BASIN)
+        for k, (bx, by) in enumerate(BLOCKS):
+            p.place(idx(world.entity(f"block_{k}")), bx, by)
+        return p

@@ -5,20 +5,22 @@ sphere-line contacts and the rod's torque — is world_step's own generic
 kernel (k_generic_physics, launched first in the same stream); k_wheel<n>
 (csrc/ss_small.cu) then does count, reward -|w - target| (float32), horizon
 done and the observation [x, y, vx, vy, rod - self, cos, sin (numpy float32),
-w, target] in one launch.  Resets run the reference's host program (agents
-scattered, the rod's angle drawn uniform in [0, 2 pi)).
+w, target] in one launch.  Resets are a device reset program (agents scattered, the rod's angle
+drawn uniform in [0, 2 pi)), masked and sharded like every built-in.
 """
 from __future__ import annotations
+
+import numpy as np
 
 from .. import _native as N
 from ..core import World
 from . import register
-from ._fused import FusedScenario, HostReset, f32
+from ._fused import FusedScenario, RefHeuristic, ResetProgram, f32
 from .catalog import Wheel as _Reference
 
 
 @register("wheel")
-class Wheel(HostReset, FusedScenario):
+class Wheel(RefHeuristic, FusedScenario):
     native_id = N.SCN_WHEEL
     max_steps = 200
     _reference = _Reference
@@ -42,3 +44,14 @@ class Wheel(HostReset, FusedScenario):
 
     def fill_constants(self, world, d):
         d.sc[0] = f32(self.target_spin)
+
+    def reset_program(self, world):
+        """wheel.py:53-59: agents scattered in [-1, 1]^2; the rod's angle
+        uniform in [0, 2 pi), its motion zeroed."""
+        p = ResetProgram()
+        for a in world.agents:
+            p.scatter(world.index_of(a), (-1.0, -1.0), (1.0, 1.0))
+        rod = world.index_of(world.entity("rod"))
+        p.setrot(rod, p.draw(0.0, 2 * np.pi))
+        p.zero(rod)
+        return p
