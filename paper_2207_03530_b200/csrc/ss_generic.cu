@@ -5,7 +5,7 @@
 // world_step() API.  One thread per env; the per-entity force/torque
 // accumulators of a warp's 32 envs live in shared memory ([E][32] each) so
 // any entity count and any pair list run through the same code.
-#include "ss_geometry.cuh"
+#include "ss_physics.cuh"
 
 namespace ss {
 
@@ -26,39 +26,6 @@ struct GenericArgs {
   int* status;   // set to 1 when an unsupported shape pair is met
 };
 
-SS_DEV V2 load_pos(const DevState& s, const SsEntityDesc& d, int64_t e) {
-  if (d.movable) { const float4 q = s.dyn[d.slot * s.B + e]; return v2(q.x, q.y); }
-  const float2 q = s.stat[d.slot * s.B + e];
-  return v2(q.x, q.y);
-}
-
-// World-frame anchor of a joint end: pos + R(rot) (ox, oy), numpy float32
-// cos/sin, separately rounded (the oracle's joint_anchor); a zero offset is
-// the position itself.
-SS_DEV V2 joint_anchor(const DevState& s, const SsEntityDesc& d, int k, int64_t e, float ox, float oy,
-                       V2& pos) {
-  pos = load_pos(s, d, e);
-  if (ox == 0.0f && oy == 0.0f) return pos;
-  const float r = s.rot[k * s.B + e].x;
-  const float c = np_cosf(r), sn = np_sinf(r);
-  return v2(fadd(pos.x, fsub(fmul(ox, c), fmul(oy, sn))), fadd(pos.y, fadd(fmul(ox, sn), fmul(oy, c))));
-}
-
-// Distance-joint penalty force on end a (SsJointDesc, include/swarmsim_b200.h);
-// false when the joint exerts no force in this env.
-SS_DEV bool joint_force(V2 pa, V2 pb, float target, float stiff, float k, float& fx, float& fy) {
-  const float dx = fsub(pa.x, pb.x), dy = fsub(pa.y, pb.y);
-  const float dist = fsqrt(fadd(fmul(dx, dx), fmul(dy, dy)));
-  if (!(dist >= 1e-6f) || dist == target) return false;
-  const bool rep = dist < target;
-  const float z = fdiv(rep ? fsub(target, dist) : fsub(dist, target), k);
-  const float pen = fmul(np_softplus(z), k);
-  const float sf = rep ? stiff : -stiff;
-  fx = fmul(fmul(sf, fdiv(dx, dist)), pen);
-  fy = fmul(fmul(sf, fdiv(dy, dist)), pen);
-  return true;
-}
-
 __global__ void __launch_bounds__(32) k_generic_physics(const GenericArgs a) {
   extern __shared__ float sm[];
   grid_dep_sync();
@@ -71,100 +38,20 @@ __global__ void __launch_bounds__(32) k_generic_physics(const GenericArgs a) {
     if (a.mode & SS_DO_COUNT) a.s.step_count[e] += 1;
     return;
   }
-  float* FX = sm;
-  float* FY = sm + a.E * 32;
-  float* TQ = sm + 2 * a.E * 32;
-  // sub-steps (PhysK.substeps, 1 = the reference): the decoded actions are
-  // held, forces re-evaluated on each sub-step's state with the sub-step dt
-  for (int sub = 0; sub < a.ph.substeps; ++sub) {
-    for (int k = 0; k < a.E; ++k) { FX[k * 32 + lane] = 0.0f; FY[k * 32 + lane] = 0.0f; TQ[k * 32 + lane] = 0.0f; }
-    // action forces (dynamics.py:151-152); decode_action (env.py:97) when flagged
-    for (int i = 0; i < a.A; ++i) {
-      if (a.act[i] == nullptr) continue;
-      const float2 u = a.act[i][e];
-      float fx = u.x, fy = u.y;
-      if ((a.decode_mask[i >> 6] >> (i & 63)) & 1ull) {
-        const SsEntityDesc& d = a.ents[i];
-        fx = fmul(clip_sym(u.x, d.u_range), d.u_mult);
-        fy = fmul(clip_sym(u.y, d.u_range), d.u_mult);
-      }
-      FX[i * 32 + lane] = fadd(0.0f, fx);
-      FY[i * 32 + lane] = fadd(0.0f, fy);
+  // action forces (dynamics.py:151-152); decode_action (env.py:97) when flagged
+  const bool ok = env_physics(a.s, a.ph, a.ents, a.pairs, a.E, a.P, a.joints, a.J, a.A, e, sm, 32, lane,
+                              [&](int i, float& fx, float& fy) {
+    if (a.act[i] == nullptr) return false;
+    const float2 u = a.act[i][e];
+    fx = u.x; fy = u.y;
+    if ((a.decode_mask[i >> 6] >> (i & 63)) & 1ull) {
+      const SsEntityDesc& d = a.ents[i];
+      fx = fmul(clip_sym(u.x, d.u_range), d.u_mult);
+      fy = fmul(clip_sym(u.y, d.u_range), d.u_mult);
     }
-    if (a.ph.has_gravity) {  // dynamics.py:154-161
-      for (int k = 0; k < a.E; ++k) {
-        const SsEntityDesc& d = a.ents[k];
-        if (!d.movable) continue;
-        FX[k * 32 + lane] = fadd(FX[k * 32 + lane], d.grav_x);
-        FY[k * 32 + lane] = fadd(FY[k * 32 + lane], d.grav_y);
-      }
-    }
-    // pair contacts in pair-list order (dynamics.py:163-180)
-    for (int p = 0; p < a.P; ++p) {
-      const SsPairDesc pr = a.pairs[p];
-      const SsEntityDesc& di = a.ents[pr.i];
-      const SsEntityDesc& dj = a.ents[pr.j];
-      const V2 pi = load_pos(a.s, di, e), pj = load_pos(a.s, dj, e);
-      const float ri = a.s.rot[pr.i * B + e].x, rj = a.s.rot[pr.j * B + e].x;
-      ShapeK si, sj;
-      si.kind = di.shape; si.d0 = di.dim0; si.d1 = di.dim1;
-      sj.kind = dj.shape; sj.d0 = dj.dim0; sj.d1 = dj.dim1;
-      V2 oi, oj;
-      if (!closest_points(pi, ri, si, pj, rj, sj, oi, oj)) { *a.status = 1; return; }
-      float fx, fy;
-      if (!contact_force(oi.x, oi.y, oj.x, oj.y, pr.d_min, pr.d2_act, pr.sign, a.ph.ck, a.ph.k, fx, fy)) continue;
-      FX[pr.i * 32 + lane] = fadd(FX[pr.i * 32 + lane], fx);
-      FY[pr.i * 32 + lane] = fadd(FY[pr.i * 32 + lane], fy);
-      FX[pr.j * 32 + lane] = fsub(FX[pr.j * 32 + lane], fx);
-      FY[pr.j * 32 + lane] = fsub(FY[pr.j * 32 + lane], fy);
-      if (di.rotatable) {
-        const V2 r = vsub(oi, pi);
-        TQ[pr.i * 32 + lane] = fadd(TQ[pr.i * 32 + lane], fsub(fmul(r.x, fy), fmul(r.y, fx)));
-      }
-      if (dj.rotatable) {
-        const V2 r = vsub(oj, pj);
-        TQ[pr.j * 32 + lane] = fsub(TQ[pr.j * 32 + lane], fsub(fmul(r.x, fy), fmul(r.y, fx)));
-      }
-    }
-    // joint constraints (extension, SsJointDesc), joint-list order
-    for (int q = 0; q < a.J; ++q) {
-      const SsJointDesc jt = a.joints[q];
-      const SsEntityDesc& da = a.ents[jt.a];
-      const SsEntityDesc& db = a.ents[jt.b];
-      V2 pa, pb;
-      const V2 qa = joint_anchor(a.s, da, jt.a, e, jt.ox_a, jt.oy_a, pa);
-      const V2 qb = joint_anchor(a.s, db, jt.b, e, jt.ox_b, jt.oy_b, pb);
-      float fx, fy;
-      if (!joint_force(qa, qb, jt.dist, jt.stiffness, a.ph.k, fx, fy)) continue;
-      FX[jt.a * 32 + lane] = fadd(FX[jt.a * 32 + lane], fx);
-      FY[jt.a * 32 + lane] = fadd(FY[jt.a * 32 + lane], fy);
-      FX[jt.b * 32 + lane] = fsub(FX[jt.b * 32 + lane], fx);
-      FY[jt.b * 32 + lane] = fsub(FY[jt.b * 32 + lane], fy);
-      if (da.rotatable && jt.rotate_a) {
-        const V2 r = vsub(qa, pa);
-        TQ[jt.a * 32 + lane] = fadd(TQ[jt.a * 32 + lane], fsub(fmul(r.x, fy), fmul(r.y, fx)));
-      }
-      if (db.rotatable && jt.rotate_b) {
-        const V2 r = vsub(qb, pb);
-        TQ[jt.b * 32 + lane] = fsub(TQ[jt.b * 32 + lane], fsub(fmul(r.x, fy), fmul(r.y, fx)));
-      }
-    }
-    // integrate (dynamics.py:182-184)
-    for (int k = 0; k < a.E; ++k) {
-      const SsEntityDesc& d = a.ents[k];
-      if (d.movable) {
-        float4 q = a.s.dyn[d.slot * B + e];
-        integrate_lin(q.x, q.y, q.z, q.w, FX[k * 32 + lane], FY[k * 32 + lane], a.ph.keep,
-                      d.inv_m_dt, a.ph.dt, d.max_speed);
-        a.s.dyn[d.slot * B + e] = q;
-      }
-      if (d.rotatable) {
-        float2 r = a.s.rot[k * B + e];
-        integrate_ang(r.x, r.y, TQ[k * 32 + lane], a.ph.keep, d.inv_i_dt, a.ph.dt);
-        a.s.rot[k * B + e] = r;
-      }
-    }
-  }
+    return true;
+  });
+  if (!ok) { *a.status = 1; return; }
   if (a.mode & SS_DO_COUNT) a.s.step_count[e] += 1;
 }
 
@@ -272,6 +159,7 @@ __global__ void __launch_bounds__(512) k_check_actions(const CheckArgs a) {
     const int64_t n4 = a.n >> 2;
     for (int i = 0; i < a.A; ++i) {
       const float4* p = reinterpret_cast<const float4*>(a.act[i]);
+      if (p == nullptr) continue;           // a script drives this agent (no raw action)
       for (int64_t k = t0; k < n4; k += stride) {
         const float4 v = __ldcs(p + k);
         bad |= isnan(v.x) | isnan(v.y) | isnan(v.z) | isnan(v.w);
@@ -280,6 +168,7 @@ __global__ void __launch_bounds__(512) k_check_actions(const CheckArgs a) {
   } else {
     for (int i = 0; i < a.A; ++i) {
       const float* p = a.act[i];
+      if (p == nullptr) continue;
       for (int64_t k = t0; k < a.n; k += stride) bad |= isnan(p[k]);
     }
   }

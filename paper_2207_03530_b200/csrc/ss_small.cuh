@@ -1,0 +1,126 @@
+// ss_small.cuh — shared pieces of the thread-per-env fused step kernels
+// (simple_spread, transport, dropout: ss_spread.cu / ss_transport.cu; the
+// line / box catalog tasks: ss_catalog.cu; flocking: ss_flocking.cu): one
+// thread per environment, the whole entity state of an env in registers for
+// the duration of the step.
+//
+// One launch does, per env (env.py:209-235 order):
+//   decode (env.py:97) -> forces: action, gravity, pair contacts in the
+//   reference's lexicographic pair order (dynamics.py:151-180) -> integrate
+//   (dynamics.py:182-184) -> post_step -> step_count += 1 -> rewards ->
+//   done | horizon -> observations.
+// HBM traffic: every state row read once and written once (float4 SoA rows,
+// env index contiguous, so each warp access is a contiguous 512 B), actions
+// read once, obs/reward/done written once (obs staged per warp in shared
+// memory and streamed out with 16-byte stores).
+//
+// Each kernel family lives in its own translation unit (parallel builds) and
+// exports a host launcher taking the SmallArgs that launch_small (ss_small.cu)
+// fills from the world descriptor.
+#pragma once
+#include <cstdlib>
+
+#include "ss_bulk.cuh"
+#include "ss_physics.cuh"    // (includes ss_geometry.cuh, ss_internal.cuh)
+
+namespace ss {
+
+constexpr int kSmallMaxAgents = 8;
+constexpr int kFlockMaxRocks = 6;
+constexpr int kSmallThreads = 128;
+// minimum resident CTAs per SM requested from ptxas (register budget)
+#ifndef SS_SMALL_MINB
+#define SS_SMALL_MINB 6   // 6 x 128 threads: <= 80 registers, best measured (tools/sweep_variants.py)
+#endif
+
+struct SmallArgs {
+  DevState s;
+  PhysK ph;
+  const SsEntityDesc* ents;
+  const SsPairDesc* pairs;
+  const float2* act[kSmallMaxAgents];
+  float* obs;
+  int64_t obs_stride;   // floats between agent blocks
+  float* rew;
+  uint8_t* done;
+  int mode;
+  int raw_forces;
+  int obs_dim;
+  int E, P;             // entities, pairs (catalog kernels' in-launch world_step)
+  int acc_off;          // floats of dynamic smem before its force accumulators
+  int64_t e_begin;      // first env handled by this launch (tail launches)
+  const int* guard;
+  int guard_n;          // guard words to OR (SsStepIO.guard_count, >= 1)
+  float sc[16];
+  double sd[8];
+  int si[8];
+  // lidar (flocking extension)
+  int n_rays;
+  double lidar_range;
+  double ray_start, ray_span;
+  int attach_rot;
+  const double* ray_dir;  // [n_rays][2] cos/sin of the base angles (numpy values)
+};
+
+// Flush one agent's staged obs rows (warp-private smem) to global memory.
+SS_DEV void warp_flush(float* __restrict__ dst, int nvalid, int O, float* __restrict__ sbuf) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+  const int n = nvalid * O;
+  if ((reinterpret_cast<uintptr_t>(dst) & 15u) != 0) {
+    for (int i = lane; i < n; i += 32) __stcs(dst + i, sbuf[i]);
+    __syncwarp();
+    return;
+  }
+  const int n4 = n >> 2;
+  float4* d4 = reinterpret_cast<float4*>(dst);
+  const float4* s4 = reinterpret_cast<const float4*>(sbuf);
+  for (int i = lane; i < n4; i += 32) __stcs(d4 + i, s4[i]);
+  for (int i = (n4 << 2) + lane; i < n; i += 32) __stcs(dst + i, sbuf[i]);
+  __syncwarp();
+}
+
+// Flush staged rows whose per-lane stride P is padded to an odd number of
+// floats (conflict-free row writes for any O).  With O % 4 == 0 each 16-byte
+// output chunk lies inside one row: 4 scalar shared loads, one float4 store.
+SS_DEV void warp_flush_padded(float* __restrict__ dst, int nvalid, int O, int P,
+                              const float* __restrict__ sbuf) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+  const int n = nvalid * O;
+  // row = floor(q / O4) through a float reciprocal: (q + 0.5) / O4 sits at
+  // least 0.5 / O4 from an integer and q <= 32 * O, so the float product
+  // (relative error < 2^-22) always truncates to the exact quotient.
+  if ((O & 3) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
+    const int O4 = O >> 2;
+    const float inv = 1.0f / (float)O4;
+    for (int q = lane; q < (n >> 2); q += 32) {
+      const int r = __float2int_rz(__fmul_rn(__int2float_rn(q) + 0.5f, inv)), j = (q - r * O4) << 2;
+      const float* s = sbuf + r * P + j;
+      __stcs(reinterpret_cast<float4*>(dst) + q, make_float4(s[0], s[1], s[2], s[3]));
+    }
+  } else {
+    const float inv = 1.0f / (float)O;
+    for (int i = lane; i < n; i += 32) {
+      const int r = __float2int_rz(__fmul_rn(__int2float_rn(i) + 0.5f, inv));
+      __stcs(dst + i, sbuf[r * P + (i - r * O)]);
+    }
+  }
+  __syncwarp();
+}
+
+// decode_action's continuous branch (env.py:96-98) unless the host already
+// produced final forces.
+SS_DEV float decode_axis(float raw, const SsEntityDesc& d, int raw_forces) {
+  return raw_forces ? raw : fmul(clip_sym(raw, d.u_range), d.u_mult);
+}
+
+// Host launchers, one per translation unit (a: filled by launch_small; grid /
+// shmem derived from it).  Each returns an SsStatus.
+int launch_spread(World& w, SmallArgs& a, cudaStream_t st);
+int launch_transport(World& w, SmallArgs& a, cudaStream_t st);
+int launch_dropout(World& w, SmallArgs& a, cudaStream_t st);
+int launch_catalog(World& w, SmallArgs& a, cudaStream_t st);
+int launch_flocking(World& w, SmallArgs& a, cudaStream_t st);
+
+}  // namespace ss

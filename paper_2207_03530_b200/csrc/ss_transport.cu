@@ -1,0 +1,265 @@
+// ss_transport.cu — fused Env.step of transport / reverse_transport
+// (scenarios/transport.py, reverse_transport.py) and dropout (dropout.py).
+#include "ss_small.cuh"
+
+namespace ss {
+
+// ---------------------------------------------------------------------------
+// transport (scenarios/transport.py): NA agents (dyn 0..NA-1), package box
+// (entity NA, dyn row NA), goal marker (entity NA+1, stat row 0).
+// Pairs, lexicographic: for i: agents j>i (sphere-sphere), then (i, package)
+// (sphere-box).  sc[0] = box half length (as f32 of the python double) ,
+// sc[1] = half width, sc[2] = f32(success_dist); the doubles are passed via
+// si-packed bits: see make_small_args.
+// ---------------------------------------------------------------------------
+// REV = 1: reverse_transport (catalog scenarios/reverse_transport.py): the
+// same world (agents inside a hollow crate), observation
+// [x, y, vx, vy, crate - self, crate vel, goal - crate] (O = 10).
+template <int NA, int REV, bool MS>
+__global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_transport(const SmallArgs a) {
+  extern __shared__ __align__(16) float smem[];
+  grid_dep_sync();
+  if (guard_tripped(a.guard, a.guard_n)) return;
+  constexpr int O = REV ? 10 : 12;
+  const int64_t B = a.s.B;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = e < B;
+  float px[NA + 1], py[NA + 1], vx[NA + 1], vy[NA + 1];
+  float gx = 0.f, gy = 0.f, prot = 0.f;
+  float2 u[NA];
+  int64_t steps = 0;
+  if (valid) {
+    // every global load of the step issued up front
+#pragma unroll
+    for (int i = 0; i <= NA; ++i) {
+      const float4 q = a.s.dyn[i * B + e];
+      px[i] = q.x; py[i] = q.y; vx[i] = q.z; vy[i] = q.w;
+    }
+    const float2 g = a.s.stat[e];
+    gx = g.x; gy = g.y;
+    if (a.mode & SS_DO_PHYSICS) {
+      prot = a.s.rot[NA * B + e].x;
+#pragma unroll
+      for (int i = 0; i < NA; ++i) u[i] = a.act[i][e];
+    }
+    if (a.mode & (SS_DO_COUNT | SS_DO_DONE)) steps = a.s.step_count[e];
+  }
+  if (valid && (a.mode & SS_DO_PHYSICS)) {
+    float ca, sa;
+    if (prot == 0.0f) { ca = 1.0f; sa = prot; } else { ca = np_cosf(prot); sa = np_sinf(prot); }
+    const double hx = a.sd[0], hy = a.sd[1];
+    // one physics sub-step: forces from `act` (decoded actions + gravity),
+    // contacts in pair order, integrate
+    auto substep = [&](const float2 (&act)[NA]) {
+      float fx[NA + 1], fy[NA + 1];
+#pragma unroll
+      for (int i = 0; i < NA; ++i) {
+        const SsEntityDesc& d = a.ents[i];
+        fx[i] = decode_axis(act[i].x, d, a.raw_forces);
+        fy[i] = decode_axis(act[i].y, d, a.raw_forces);
+      }
+      fx[NA] = 0.0f; fy[NA] = 0.0f;
+      if (a.ph.has_gravity) {
+#pragma unroll
+        for (int i = 0; i <= NA; ++i) {
+          fx[i] = fadd(fx[i], a.ents[i].grav_x); fy[i] = fadd(fy[i], a.ents[i].grav_y);
+        }
+      }
+      int p = 0;
+#pragma unroll
+      for (int i = 0; i < NA; ++i) {
+#pragma unroll
+        for (int j = i + 1; j < NA; ++j, ++p) {
+          const SsPairDesc pr = a.pairs[p];
+          float cx, cy;
+          if (contact_force(px[i], py[i], px[j], py[j], pr.d_min, pr.d2_act, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
+            fx[i] = fadd(fx[i], cx); fy[i] = fadd(fy[i], cy);
+            fx[j] = fsub(fx[j], cx); fy[j] = fsub(fy[j], cy);
+          }
+        }
+        {  // agent i vs package (sphere-box)
+          const SsPairDesc pr = a.pairs[p++];
+          float qx, qy, cx, cy;
+          closest_point_on_box(px[i], py[i], px[NA], py[NA], ca, sa, hx, hy, qx, qy);
+          if (contact_force(px[i], py[i], qx, qy, pr.d_min, pr.d2_act, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
+            fx[i] = fadd(fx[i], cx); fy[i] = fadd(fy[i], cy);
+            fx[NA] = fsub(fx[NA], cx); fy[NA] = fsub(fy[NA], cy);
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i <= NA; ++i) {
+        const SsEntityDesc& d = a.ents[i];
+        integrate_lin(px[i], py[i], vx[i], vy[i], fx[i], fy[i], a.ph.keep, d.inv_m_dt, a.ph.dt,
+                      d.max_speed);
+      }
+    };
+    substep(u);
+    // further physics sub-steps (PhysK.substeps > 1: the MS instantiation,
+    // so the reference's single step keeps its register budget) reload the
+    // held actions instead of keeping them live across the first one
+    if (MS) for (int sub = 1; sub < a.ph.substeps; ++sub) {
+      float2 ur[NA];
+#pragma unroll
+      for (int i = 0; i < NA; ++i) ur[i] = a.act[i][e];
+      substep(ur);
+    }
+#pragma unroll
+    for (int i = 0; i <= NA; ++i) a.s.dyn[i * B + e] = make_float4(px[i], py[i], vx[i], vy[i]);
+  }
+  if (valid && (a.mode & SS_DO_COUNT)) { steps += 1; a.s.step_count[e] = steps; }
+  if (valid && (a.mode & (SS_DO_REWARD | SS_DO_DONE))) {
+    const float gap = norm2(fsub(px[NA], gx), fsub(py[NA], gy));
+    if (a.mode & SS_DO_REWARD) {
+#pragma unroll
+      for (int i = 0; i < NA; ++i) __stcs(a.rew + i * B + e, -gap);
+    }
+    if (a.mode & SS_DO_DONE) a.done[e] = (uint8_t)((gap < a.sc[2]) | (steps >= a.ph.max_steps));
+  }
+  if (a.mode & SS_DO_OBS) {
+    float* sbuf = smem + (threadIdx.x >> 5) * (32 * O);
+    float* row = sbuf + (threadIdx.x & 31) * O;
+    const int64_t e0 = e - (threadIdx.x & 31);
+    const int nvalid = (int)min((int64_t)32, B - e0);
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      if (valid) {
+        row[0] = px[i]; row[1] = py[i]; row[2] = vx[i]; row[3] = vy[i];
+        row[4] = fsub(px[NA], px[i]); row[5] = fsub(py[NA], py[i]);
+        if (REV) {
+          row[6] = vx[NA]; row[7] = vy[NA];
+          row[8] = fsub(gx, px[NA]); row[9] = fsub(gy, py[NA]);
+        } else {
+          row[6] = fsub(gx, px[i]); row[7] = fsub(gy, py[i]);
+          row[8] = fsub(px[NA], gx); row[9] = fsub(py[NA], gy);
+          row[10] = vx[NA]; row[11] = vy[NA];
+        }
+      }
+      if (nvalid > 0) warp_flush(a.obs + i * a.obs_stride + e0 * O, nvalid, O, sbuf);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// dropout (catalog scenarios/dropout.py): NA non-collidable agents (dyn
+// 0..NA-1), goal marker (stat row 0); no pairs.  Reward (shared):
+// float64(any agent within reach) - energy_coeff * spent, spent = the float64
+// sum over agents, in order, of fx*fx then fy*fy (float32 squares of the
+// decoded actions, promoted); done = reached.  spent is kept in flag words 0
+// and 1 (double bits) so a reward-only launch sees the last step's value.
+// sc[3] = squared bound of f32(reach); sd[0] = energy_coeff.
+// Observation: [x, y, vx, vy, goal - self, (other - self)].
+// ---------------------------------------------------------------------------
+template <int NA>
+__global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_dropout(const SmallArgs a) {
+  extern __shared__ __align__(16) float smem[];
+  grid_dep_sync();
+  if (guard_tripped(a.guard, a.guard_n)) return;
+  constexpr int O = 4 + 2 * NA;
+  const int64_t B = a.s.B;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = e < B;
+  float px[NA], py[NA], vx[NA], vy[NA];
+  float2 u[NA];
+  float gx = 0.f, gy = 0.f;
+  int64_t steps = 0;
+  uint32_t lo = 0u, hi = 0u;
+  if (valid) {
+    // every global load of the step issued up front
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      const float4 q = a.s.dyn[i * B + e];
+      px[i] = q.x; py[i] = q.y; vx[i] = q.z; vy[i] = q.w;
+    }
+    const float2 g = a.s.stat[e];
+    gx = g.x; gy = g.y;
+    if (a.mode & SS_DO_PHYSICS) {
+#pragma unroll
+      for (int i = 0; i < NA; ++i) u[i] = a.act[i][e];
+    } else if (a.mode & SS_DO_REWARD) {
+      lo = a.s.flags[e];
+      hi = a.s.flags[B + e];
+    }
+    if (a.mode & (SS_DO_COUNT | SS_DO_DONE)) steps = a.s.step_count[e];
+  }
+  double spent = __hiloint2double((int)hi, (int)lo);
+  if (valid && (a.mode & SS_DO_PHYSICS)) {
+    spent = 0.0;
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      const SsEntityDesc& d = a.ents[i];
+      float fx = decode_axis(u[i].x, d, a.raw_forces), fy = decode_axis(u[i].y, d, a.raw_forces);
+      spent = dadd_rn(dadd_rn(spent, (double)fmul(fx, fx)), (double)fmul(fy, fy));
+      if (a.ph.has_gravity) { fx = fadd(fx, d.grav_x); fy = fadd(fy, d.grav_y); }
+      for (int sub = 0; sub < a.ph.substeps; ++sub)   // no pairs: sub-steps are independent
+        integrate_lin(px[i], py[i], vx[i], vy[i], fx, fy, a.ph.keep, d.inv_m_dt, a.ph.dt, d.max_speed);
+      a.s.dyn[i * B + e] = make_float4(px[i], py[i], vx[i], vy[i]);
+    }
+    a.s.flags[e] = (uint32_t)__double2loint(spent);
+    a.s.flags[B + e] = (uint32_t)__double2hiint(spent);
+  }
+  if (valid && (a.mode & SS_DO_COUNT)) { steps += 1; a.s.step_count[e] = steps; }
+  bool reached = false;
+  if (valid) {
+#pragma unroll
+    for (int i = 0; i < NA; ++i) reached |= sqnorm(fsub(px[i], gx), fsub(py[i], gy)) <= a.sc[3];
+  }
+  if (valid && (a.mode & SS_DO_REWARD)) {
+    const float r = (float)dsub_rn(reached ? 1.0 : 0.0, dmul_rn(a.sd[0], spent));
+#pragma unroll
+    for (int i = 0; i < NA; ++i) __stcs(a.rew + i * B + e, r);
+  }
+  if (valid && (a.mode & SS_DO_DONE)) a.done[e] = (uint8_t)(reached | (steps >= a.ph.max_steps));
+  if (a.mode & SS_DO_OBS) {
+    float* sbuf = smem + (threadIdx.x >> 5) * (32 * O);
+    float* row = sbuf + (threadIdx.x & 31) * O;
+    const int64_t e0 = e - (threadIdx.x & 31);
+    const int nvalid = (int)min((int64_t)32, B - e0);
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      if (valid) {
+        row[0] = px[i]; row[1] = py[i]; row[2] = vx[i]; row[3] = vy[i];
+        row[4] = fsub(gx, px[i]); row[5] = fsub(gy, py[i]);
+        int c = 6;
+#pragma unroll
+        for (int o = 0; o < NA; ++o) {
+          if (o == i) continue;
+          row[c++] = fsub(px[o], px[i]); row[c++] = fsub(py[o], py[i]);
+        }
+      }
+      if (nvalid > 0) warp_flush(a.obs + i * a.obs_stride + e0 * O, nvalid, O, sbuf);
+    }
+  }
+}
+
+int launch_transport(World& w, SmallArgs& a, cudaStream_t st) {
+  const int NA = w.d.n_agents;
+  const bool ms = a.ph.substeps > 1;
+  const unsigned grid = (unsigned)((w.d.batch + kSmallThreads - 1) / kSmallThreads);
+  const size_t shmem = (size_t)kSmallThreads * w.d.obs_dim * sizeof(float);
+#define SS_CASE(n)                                                                                   \
+  case n:                                                                                            \
+    if (ms) {                                                                                        \
+      if (w.d.si[1]) launch_step(k_transport<n, 1, true>, dim3(grid), dim3(kSmallThreads), shmem, st, a); \
+      else launch_step(k_transport<n, 0, true>, dim3(grid), dim3(kSmallThreads), shmem, st, a);           \
+    } else {                                                                                         \
+      if (w.d.si[1]) launch_step(k_transport<n, 1, false>, dim3(grid), dim3(kSmallThreads), shmem, st, a); \
+      else launch_step(k_transport<n, 0, false>, dim3(grid), dim3(kSmallThreads), shmem, st, a);           \
+    }                                                                                                \
+    break;
+  switch (NA) { SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) }
+#undef SS_CASE
+  return cuda_status(cudaGetLastError(), "transport step launch");
+}
+
+int launch_dropout(World& w, SmallArgs& a, cudaStream_t st) {
+  const int NA = w.d.n_agents;
+  const unsigned grid = (unsigned)((w.d.batch + kSmallThreads - 1) / kSmallThreads);
+  const size_t shmem = (size_t)kSmallThreads * w.d.obs_dim * sizeof(float);
+#define SS_CASE(n) case n: launch_step(k_dropout<n>, dim3(grid), dim3(kSmallThreads), shmem, st, a); break;
+  switch (NA) { SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) }
+#undef SS_CASE
+  return cuda_status(cudaGetLastError(), "dropout step launch");
+}
+
+}  // namespace ss

@@ -54,6 +54,11 @@ class Scenario:
     def heuristic_action(self, agent_index: int, obs):
         raise NotImplementedError
 
+    def device_scripted(self, agent: Agent) -> bool:
+        """True when the scenario's fused kernel runs this agent's
+        action_script itself (no host decode, no raw action needed)."""
+        return False
+
 
 @dataclass(frozen=True)
 class ActionSpec:
@@ -266,7 +271,7 @@ class Env:
         if isinstance(raw_actions, torch.Tensor) and raw_actions.ndim == 3:
             if (self.fused and raw_actions.device == self.device and raw_actions.dtype == torch.float32
                     and tuple(raw_actions.shape) == (len(agents), self.batch_size, 2)
-                    and raw_actions.is_contiguous() and not self._needs_host_decode([0] * len(agents))
+                    and raw_actions.is_contiguous() and not self._needs_host_decode([0] * len(agents), True)
                     and all(s.comm_dim == 0 for s in self.action_specs)):
                 base, stride = raw_actions.data_ptr(), self.batch_size * 8
                 return self._step_fused_ptrs([base + a * stride for a in range(len(agents))], raw_actions, False)
@@ -281,10 +286,15 @@ class Env:
         return self._step_generic(raw_actions)
 
     def _fast_actions(self, raw_actions):
-        """Continuous, noiseless, unscripted: raw (B, 2) device tensors, no decode on host."""
+        """Continuous, noiseless, unscripted (or kernel-scripted): raw (B, 2)
+        device tensors, no decode on host; None for a kernel-scripted agent
+        given no action."""
         B, dev = self.batch_size, self.device
         out = []
         for raw, agent, spec in zip(raw_actions, self.agents, self.action_specs):
+            if raw is None:
+                out.append(None)
+                continue
             t = _to_device(raw, dev)
             if t.ndim == 1 and spec.comm_dim == 0 and tuple(t.shape) == (2,) and B == 1:
                 t = t.reshape(1, 2)
@@ -319,18 +329,24 @@ class Env:
             forces.append(torch.stack([act.force.x, act.force.y], 1).to(self.device, torch.float32).contiguous())
         return forces
 
-    def _needs_host_decode(self, raw_actions) -> bool:
+    def _needs_host_decode(self, raw_actions, all_given: bool = False) -> bool:
         if self.action_mode != "continuous":
             return True
+        sc = self.scenario
         for raw, agent in zip(raw_actions, self.agents):
-            if raw is None or agent.action_script is not None or agent.action_noise_std > 0.0:
+            if agent.action_noise_std > 0.0:
+                return True
+            if agent.action_script is not None:
+                if not (self.fused and sc.device_scripted(agent)):
+                    return True
+            elif raw is None and not all_given:
                 return True
         return False
 
     def _step_fused(self, raw_actions) -> StepResult:
         raw = self._needs_host_decode(raw_actions)
         forces = self._host_decoded(raw_actions) if raw else self._fast_actions(raw_actions)
-        return self._step_fused_ptrs([f.data_ptr() for f in forces], forces, raw)
+        return self._step_fused_ptrs([None if f is None else f.data_ptr() for f in forces], forces, raw)
 
     def _step_fused_ptrs(self, ptrs, keepalive, raw: bool) -> StepResult:
         world, sc = self.world, self.scenario
@@ -346,7 +362,7 @@ class Env:
                                    flip_rng=False, stream=st)
         if guard is not None and int(self._flag.item()) != 0:
             forces = keepalive if isinstance(keepalive, list) else list(keepalive.unbind(0))
-            bad = next(a.name for a, f in zip(self.agents, forces) if bool(torch.isnan(f).any()))
+            bad = next(a.name for a, f in zip(self.agents, forces) if f is not None and bool(torch.isnan(f).any()))
             raise ContractViolation(f"action for '{bad}' contains NaN")
         if sc.advances_rng_per_step:
             world.rng.flip()

@@ -32,9 +32,6 @@ class Balance(RefHeuristic, FusedScenario):
     def obs_dim(self, world):
         return 17
 
-    def physics_fused(self, world) -> bool:
-        return False         # world_step's generic kernel, then k_balance
-
     def template_pairs(self, world):
         return list(world.collidable_pairs())
 

@@ -16,7 +16,7 @@ from .. import _native as N
 from ..core import World
 from . import register
 from ._fused import FusedScenario, RefHeuristic, ResetProgram, f32
-from .catalog import FIELD_HX, Football as _Reference
+from .catalog import FIELD_HX, Football as _Reference, chase_script
 
 
 @register("football")
@@ -34,11 +34,13 @@ class Football(RefHeuristic, FusedScenario):
     def obs_dim(self, world):
         return 8 + 2 * (len(world.agents) - 1) + 2
 
-    def physics_fused(self, world) -> bool:
-        return False         # world_step's generic kernel, then k_football
-
     def template_pairs(self, world):
         return list(world.collidable_pairs())
+
+    def device_scripted(self, agent) -> bool:
+        """The reds' chase script runs inside k_football (same float32
+        arithmetic as catalog.chase_script / football.py:31-47)."""
+        return agent.action_script is chase_script
 
     def fill_constants(self, world, d):
         d.sc[0] = f32(FIELD_HX + 0.04)     # _scored thresholds (python double)

@@ -34,9 +34,6 @@ class GiveWay(RefHeuristic, FusedScenario):
     def obs_dim(self, world):
         return 12
 
-    def physics_fused(self, world) -> bool:
-        return False         # world_step's generic kernel, then k_give_way
-
     def template_pairs(self, world):
         return list(world.collidable_pairs())
 

@@ -32,9 +32,6 @@ class Passage(RefHeuristic, FusedScenario):
     def obs_dim(self, world):
         return 10 + 2 * (len(world.agents) - 1)
 
-    def physics_fused(self, world) -> bool:
-        return False         # world_step's generic kernel, then k_passage
-
     def template_pairs(self, world):
         return list(world.collidable_pairs())
 

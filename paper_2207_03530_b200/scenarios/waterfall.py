@@ -32,9 +32,6 @@ class Waterfall(RefHeuristic, FusedScenario):
     def obs_dim(self, world):
         return 6 + 2 * len(BLOCKS)
 
-    def physics_fused(self, world) -> bool:
-        return False         # world_step's generic kernel, then k_waterfall
-
     def template_pairs(self, world):
         return list(world.collidable_pairs())
 

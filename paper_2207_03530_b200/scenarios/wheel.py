@@ -36,9 +36,6 @@ class Wheel(RefHeuristic, FusedScenario):
     def obs_dim(self, world):
         return 10
 
-    def physics_fused(self, world) -> bool:
-        return False         # world_step's generic kernel, then k_wheel
-
     def template_pairs(self, world):
         return list(world.collidable_pairs())
 

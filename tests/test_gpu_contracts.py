@@ -80,13 +80,66 @@ def test_nan_guard_on_generic_physics(cuda, name):
     assert torch.equal(e.step_count, steps)
 
 
-@pytest.mark.parametrize("name", ["wheel", "football"])
-def test_host_reset_refuses_sharding(cuda, name):
-    sc = S.create_scenario(name)
-    if getattr(sc, "shardable_reset", False):
-        pytest.skip(f"{name} resets on the device")
+class _HostResetTask(S.Scenario):
+    """A user scenario with a host reset program (numpy draws from the Env stream)."""
+
+    def make_world(self, B, rng):
+        w = S.World(B, rng=rng, device=getattr(rng, "device", None))
+        w.add(S.Agent("a", S.Sphere(0.05)))
+        return w
+
+    def reset_world_at(self, world, env_index=None):
+        n = 1 if env_index is not None else world.batch_size
+        world.entity("a").state.set_pos_xy(world.rng.uniform(-1, 1, (n,)), world.rng.uniform(-1, 1, (n,)),
+                                           env_index)
+
+    def reward(self, agent, world):
+        return torch.zeros(world.batch_size, device=world.device)
+
+    def observation(self, agent, world):
+        return torch.stack([agent.state.pos.x, agent.state.pos.y], 1)
+
+
+def test_host_reset_refuses_sharding(cuda):
     with pytest.raises(S.ContractViolation, match="shard"):
-        S.Env(sc, 8, device=cuda, env_offset=8, global_batch=16)
+        S.Env(_HostResetTask(), 8, device=cuda, env_offset=8, global_batch=16)
+
+
+@pytest.mark.parametrize("name", ["wheel", "balance", "give_way", "passage", "waterfall", "football",
+                                  "reverse_transport"])
+def test_catalog_shards_equal_unsharded(cuda, name):
+    """Device reset programs draw at global env indices: two shards of a
+    catalog task (incl. a sharded masked reset) equal the unsharded run."""
+    from paper_2207_03530_b200.parallel import shard_range
+
+    Bg = 77
+    full = S.Env(S.create_scenario(name), Bg, seed=4, device=cuda)
+    shards = []
+    for r in range(2):
+        off, cnt = shard_range(r, 2, Bg)
+        shards.append((off, cnt, S.Env(S.create_scenario(name), cnt, seed=4, device=cuda,
+                                       env_offset=off, global_batch=Bg)))
+    for off, cnt, e in shards:
+        np.testing.assert_array_equal(state(e), state(full)[:, :, off:off + cnt])
+    plans = G.pregen_actions(len(full.agents), Bg, 12, 5)
+    mask = np.zeros(Bg, dtype=bool)
+    mask[[0, 3, 38, 39, 40, 76]] = True
+    for t, plan in enumerate(plans):
+        raw = [None if a.action_script is not None else p for a, p in zip(full.agents, plan)]
+        full.step(raw)
+        for off, cnt, e in shards:
+            e.step([None if p is None else p[off:off + cnt] for p in raw])
+        if t == 5:
+            full.reset_at(torch.from_numpy(mask).to(cuda))
+            base = 0
+            total = torch.tensor([int(mask.sum())], device=cuda)
+            for off, cnt, e in shards:
+                m = torch.from_numpy(mask[off:off + cnt]).to(cuda)
+                e.scenario.reset_world_masked(e.world, m, torch.tensor([base], device=cuda), total)
+                e.world.step_count[m] = 0
+                base += int(mask[off:off + cnt].sum())
+    for off, cnt, e in shards:
+        np.testing.assert_array_equal(state(e), state(full)[:, :, off:off + cnt])
 
 
 def test_reset_at_selectors(cuda):
