@@ -247,14 +247,10 @@ SS_DEV void agents_physics(const LargeArgs& a, float2* pos, float2* vel, int64_t
         integrate_lin(px[t], py[t], vx[t], vy[t], fx[t], fy[t], a.ph.keep, d.inv_m_dt, a.ph.dt,
                       d.max_speed);
         pos[k] = make_float2(px[t], py[t]);
+        if (sub + 1 == a.ph.substeps) a.s.dyn[k * B + e] = make_float4(px[t], py[t], vx[t], vy[t]);
       }
     }
     __syncwarp();   // sub-step positions staged before the next sub-step reads them
-    }
-#pragma unroll
-    for (int t = 0; t < T; ++t) {
-      const int k = lane + 32 * t;
-      if (k < a.NA) a.s.dyn[k * B + e] = make_float4(px[t], py[t], vx[t], vy[t]);
     }
   }
 #pragma unroll

@@ -80,6 +80,48 @@ SS_DEV void warp_flush(float* __restrict__ dst, int nvalid, int O, float* __rest
   __syncwarp();
 }
 
+// Observation flush through the bulk-copy engine (SS_OBS_BULK): each agent's
+// 32 staged rows have their own staging block, so a full, 16-byte aligned
+// warp block leaves with ONE cp.async.bulk store issued by lane 0 (the LSU
+// and the other lanes are free at once); partial blocks take warp_flush.
+// obs_bulk_drain() must run before the kernel exits (smem is read async).
+#ifndef SS_OBS_BULK
+#define SS_OBS_BULK 1   // measured: transport 1M envs 128 -> 118 us, simple_spread 59.3 -> 58.6 us
+#endif
+constexpr int kObsBulk = SS_OBS_BULK;
+
+SS_DEV void warp_flush_bulk(float* __restrict__ dst, int nvalid, int O, float* __restrict__ sbuf) {
+  const uint32_t bytes = (uint32_t)(nvalid * O) * 4u;
+  if (nvalid == 32 && (bytes & 15u) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
+    fence_proxy_async_smem();      // this lane's row -> visible to the async proxy
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+      bulk_store(dst, sbuf, bytes);
+      bulk_commit();
+    }
+    return;
+  }
+  warp_flush(dst, nvalid, O, sbuf);
+}
+
+SS_DEV void obs_bulk_drain() {
+  if (kObsBulk && (threadIdx.x & 31) == 0) bulk_wait_read_all();
+}
+
+// Staging block of (warp, agent i): one per agent with SS_OBS_BULK.
+SS_DEV float* obs_stage(float* smem, int i, int NA, int O) {
+  return smem + ((threadIdx.x >> 5) * (kObsBulk ? NA : 1) + (kObsBulk ? i : 0)) * (32 * O);
+}
+
+SS_DEV void obs_flush(float* __restrict__ dst, int nvalid, int O, float* __restrict__ sbuf) {
+  if (kObsBulk) warp_flush_bulk(dst, nvalid, O, sbuf);
+  else warp_flush(dst, nvalid, O, sbuf);
+}
+
+inline size_t obs_stage_bytes(int NA, int O) {
+  return (size_t)kSmallThreads * O * sizeof(float) * (kObsBulk ? NA : 1);
+}
+
 // Flush staged rows whose per-lane stride P is padded to an odd number of
 // floats (conflict-free row writes for any O).  With O % 4 == 0 each 16-byte
 // output chunk lies inside one row: 4 scalar shared loads, one float4 store.

@@ -137,15 +137,18 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_simple_spread(
   }
   if (valid && (a.mode & SS_DO_DONE)) a.done[e] = (uint8_t)(steps >= a.ph.max_steps);
   if (a.mode & SS_DO_OBS) {
-    float* sbuf = smem + (threadIdx.x >> 5) * (32 * O);
-    float* row = sbuf + (threadIdx.x & 31) * O;
+    float* sbuf = nullptr;
+    float* row = nullptr;
     const int64_t e0 = e - (threadIdx.x & 31);
     const int nvalid = (int)min((int64_t)32, B - e0);
 #pragma unroll
     for (int i = 0; i < NA; ++i) {
+      sbuf = obs_stage(smem, i, NA, O);
+      row = sbuf + (threadIdx.x & 31) * O;
       if (valid) v.obs_row(i, row);
-      if (nvalid > 0) warp_flush(a.obs + i * a.obs_stride + e0 * O, nvalid, O, sbuf);
+      if (nvalid > 0) obs_flush(a.obs + i * a.obs_stride + e0 * O, nvalid, O, sbuf);
     }
+    obs_bulk_drain();
   }
 }
 
@@ -301,7 +304,7 @@ int launch_spread(World& w, SmallArgs& a, cudaStream_t st) {
   const int NA = w.d.n_agents;
   const int64_t B = w.d.batch;
   const bool ms = a.ph.substeps > 1;   // sub-stepped physics: the MS kernel instantiations
-  const size_t shmem = (size_t)kSmallThreads * w.d.obs_dim * sizeof(float);
+  const size_t shmem = obs_stage_bytes(w.d.n_agents, w.d.obs_dim);
   // full steps on tile-aligned data go through the bulk-copy pipeline;
   // the (< 128 env) tail and every other mode through the eager kernel
   int64_t ntiles = 0;

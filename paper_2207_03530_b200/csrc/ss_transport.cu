@@ -92,6 +92,9 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_transport(cons
         const SsEntityDesc& d = a.ents[i];
         integrate_lin(px[i], py[i], vx[i], vy[i], fx[i], fy[i], a.ph.keep, d.inv_m_dt, a.ph.dt,
                       d.max_speed);
+        // single step: store each row as soon as it is final (the LSU drains
+        // the stores while the next entity integrates)
+        if (!MS) a.s.dyn[i * B + e] = make_float4(px[i], py[i], vx[i], vy[i]);
       }
     };
     substep(u);
@@ -104,8 +107,10 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_transport(cons
       for (int i = 0; i < NA; ++i) ur[i] = a.act[i][e];
       substep(ur);
     }
+    if (MS) {
 #pragma unroll
-    for (int i = 0; i <= NA; ++i) a.s.dyn[i * B + e] = make_float4(px[i], py[i], vx[i], vy[i]);
+      for (int i = 0; i <= NA; ++i) a.s.dyn[i * B + e] = make_float4(px[i], py[i], vx[i], vy[i]);
+    }
   }
   if (valid && (a.mode & SS_DO_COUNT)) { steps += 1; a.s.step_count[e] = steps; }
   if (valid && (a.mode & (SS_DO_REWARD | SS_DO_DONE))) {
@@ -117,12 +122,14 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_transport(cons
     if (a.mode & SS_DO_DONE) a.done[e] = (uint8_t)((gap < a.sc[2]) | (steps >= a.ph.max_steps));
   }
   if (a.mode & SS_DO_OBS) {
-    float* sbuf = smem + (threadIdx.x >> 5) * (32 * O);
-    float* row = sbuf + (threadIdx.x & 31) * O;
+    float* sbuf = nullptr;
+    float* row = nullptr;
     const int64_t e0 = e - (threadIdx.x & 31);
     const int nvalid = (int)min((int64_t)32, B - e0);
 #pragma unroll
     for (int i = 0; i < NA; ++i) {
+      sbuf = obs_stage(smem, i, NA, O);
+      row = sbuf + (threadIdx.x & 31) * O;
       if (valid) {
         row[0] = px[i]; row[1] = py[i]; row[2] = vx[i]; row[3] = vy[i];
         row[4] = fsub(px[NA], px[i]); row[5] = fsub(py[NA], py[i]);
@@ -135,8 +142,9 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_transport(cons
           row[10] = vx[NA]; row[11] = vy[NA];
         }
       }
-      if (nvalid > 0) warp_flush(a.obs + i * a.obs_stride + e0 * O, nvalid, O, sbuf);
+      if (nvalid > 0) obs_flush(a.obs + i * a.obs_stride + e0 * O, nvalid, O, sbuf);
     }
+    obs_bulk_drain();
   }
 }
 
@@ -211,12 +219,14 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_dropout(const 
   }
   if (valid && (a.mode & SS_DO_DONE)) a.done[e] = (uint8_t)(reached | (steps >= a.ph.max_steps));
   if (a.mode & SS_DO_OBS) {
-    float* sbuf = smem + (threadIdx.x >> 5) * (32 * O);
-    float* row = sbuf + (threadIdx.x & 31) * O;
+    float* sbuf = nullptr;
+    float* row = nullptr;
     const int64_t e0 = e - (threadIdx.x & 31);
     const int nvalid = (int)min((int64_t)32, B - e0);
 #pragma unroll
     for (int i = 0; i < NA; ++i) {
+      sbuf = obs_stage(smem, i, NA, O);
+      row = sbuf + (threadIdx.x & 31) * O;
       if (valid) {
         row[0] = px[i]; row[1] = py[i]; row[2] = vx[i]; row[3] = vy[i];
         row[4] = fsub(gx, px[i]); row[5] = fsub(gy, py[i]);
@@ -227,8 +237,9 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_dropout(const 
           row[c++] = fsub(px[o], px[i]); row[c++] = fsub(py[o], py[i]);
         }
       }
-      if (nvalid > 0) warp_flush(a.obs + i * a.obs_stride + e0 * O, nvalid, O, sbuf);
+      if (nvalid > 0) obs_flush(a.obs + i * a.obs_stride + e0 * O, nvalid, O, sbuf);
     }
+    obs_bulk_drain();
   }
 }
 
@@ -236,7 +247,7 @@ int launch_transport(World& w, SmallArgs& a, cudaStream_t st) {
   const int NA = w.d.n_agents;
   const bool ms = a.ph.substeps > 1;
   const unsigned grid = (unsigned)((w.d.batch + kSmallThreads - 1) / kSmallThreads);
-  const size_t shmem = (size_t)kSmallThreads * w.d.obs_dim * sizeof(float);
+  const size_t shmem = obs_stage_bytes(w.d.n_agents, w.d.obs_dim);
 #define SS_CASE(n)                                                                                   \
   case n:                                                                                            \
     if (ms) {                                                                                        \
@@ -255,7 +266,7 @@ int launch_transport(World& w, SmallArgs& a, cudaStream_t st) {
 int launch_dropout(World& w, SmallArgs& a, cudaStream_t st) {
   const int NA = w.d.n_agents;
   const unsigned grid = (unsigned)((w.d.batch + kSmallThreads - 1) / kSmallThreads);
-  const size_t shmem = (size_t)kSmallThreads * w.d.obs_dim * sizeof(float);
+  const size_t shmem = obs_stage_bytes(w.d.n_agents, w.d.obs_dim);
 #define SS_CASE(n) case n: launch_step(k_dropout<n>, dim3(grid), dim3(kSmallThreads), shmem, st, a); break;
   switch (NA) { SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) }
 #undef SS_CASE

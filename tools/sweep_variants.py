@@ -1,6 +1,6 @@
 """Time the fused step kernel of each workload for several library variants.
 
-    python tools/sweep_variants.py LIB [LIB ...]
+    [SWEEP_WORKLOADS=a,b] [SWEEP_ENVS=transport=1000000,...] python tools/sweep_variants.py LIB [LIB ...]
 
 Each LIB is loaded in a fresh subprocess (SS_LIB_PATH) and every workload
 is stepped with device-resident actions; prints the median per-launch time
@@ -23,6 +23,7 @@ from paper_2207_03530_b200 import Env, create_scenario
 out = {}
 for name in %(names)r:
     scen, ov, B = WORKLOADS[name][:3]
+    B = %(envs)r.get(name, B)
     env = Env(create_scenario(scen, **ov), B, seed=0, device="cuda:0", validate=False)
     A = len(env.agents); O = env.observations()[0].shape[1]
     acts = [torch.rand((A, B, 2), device="cuda:0") * 2 - 1 for _ in range(2)]
@@ -51,7 +52,9 @@ def main() -> None:
     names = os.environ.get("SWEEP_WORKLOADS", "simple_spread,transport,flocking,dispersion,discovery").split(",")
     for lib in libs:
         env = dict(os.environ, SS_LIB_PATH=str(Path(lib).resolve()))
-        code = CHILD.replace("%(root)r", repr(str(ROOT))).replace("%(names)r", repr(names))
+        envs = dict((kv.split("=")[0], int(kv.split("=")[1])) for kv in os.environ.get("SWEEP_ENVS", "").split(",") if kv)
+        code = (CHILD.replace("%(root)r", repr(str(ROOT))).replace("%(names)r", repr(names))
+                .replace("%(envs)r", repr(envs)))
         res = subprocess.run([sys.executable, "-c", code],
                              env=env, capture_output=True, text=True)
         line = next((l for l in res.stdout.splitlines() if l.startswith("RESULT ")), None)
