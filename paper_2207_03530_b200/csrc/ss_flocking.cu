@@ -174,7 +174,7 @@ struct FlockLidarK {
   int fan_ok;   // uniform fan usable (else the per-ray screen)
 };
 
-constexpr int kLidarQueue = 64;    // (lane, target, ray) tests staged per warp and round
+constexpr int kLidarQueue = 128;   // (lane, target, ray) tests staged per warp and round
 
 // Lidar of agent i for the 32 envs of one warp (k_flocking_w), load-balanced
 // across lanes: each lane screens its env's targets with ray_window, the
@@ -189,7 +189,8 @@ constexpr int kLidarQueue = 64;    // (lane, target, ray) tests staged per warp 
 template <int NA>
 SS_DEV void lidar_fan_warp(bool active, int i, int lane, int NO, float mex, float mey,
                            const float2* spos, const float2* sst, const FlockLidarK& lk,
-                           const double2* sdird, uint32_t* best, int P, uint32_t* queue, int n_rays) {
+                           const double2* sdird, uint32_t* best, int P, uint32_t* queue, int n_rays,
+                           uint32_t init_bits) {
   constexpr int NT = NA - 1 + kFlockMaxRocks;
   uint32_t mk[NT];
   int cnt = 0;
@@ -209,7 +210,9 @@ SS_DEV void lidar_fan_warp(bool active, int i, int lane, int NO, float mex, floa
       cnt += __popc(mk[t]);
     }
   }
-  for (int m = 0; m < n_rays; ++m) best[lane * P + m] = 0x7f800000u;   // +inf
+  // minima start at float(max_range): min(float(R), float(t)...) ==
+  // float(min(R, t...)) (rounding is monotone), so the cap is folded in
+  for (int m = 0; m < n_rays; ++m) best[lane * P + m] = init_bits;
   int incl = cnt;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -474,18 +477,21 @@ __global__ void __launch_bounds__(32 * NA, (SS_FLOCK_WARPS / NA < 32 ? SS_FLOCK_
   const int64_t e = e0 + lane;
   const bool valid = e < B;
   const int nvalid = (int)min((int64_t)32, B - e0);
-  // shared memory: [dirs: n_rays double2][agents: NA x 32 float4 pre-step]
-  //                [agents: NA x 32 float2 post-step positions][queue: NA x kLidarQueue u32]
-  //                [dirs: n_rays(+1) float2][static: (1+NO) x 32 float2][rows: NA warps x 32 x P]
-  // (pre / post copies: one barrier between physics and the rest; the lidar
-  // minima are accumulated in the rows' lidar columns)
+  // shared memory: [dirs: n_rays double2][agents: NA x 32 float2 post-step positions]
+  //                [queue: NA x kLidarQueue u32][dirs: n_rays(+1) float2]
+  //                [static: (1+NO) x 32 float2][rows: NA warps x 32 x P]
+  // The pre-step agent copy (NA x 32 float4, read only by the physics)
+  // aliases the start of the rows region, which is first written after the
+  // barrier that ends the physics.  (pre / post copies: one barrier between
+  // physics and the rest; the lidar minima live in the rows' lidar columns)
   double2* sdird = reinterpret_cast<double2*>(smem_w);
-  float4* sag = reinterpret_cast<float4*>(sdird + a.n_rays);
-  float2* spos = reinterpret_cast<float2*>(sag + NA * 32);
+  float2* spos = reinterpret_cast<float2*>(sdird + a.n_rays);
   uint32_t* squeue = reinterpret_cast<uint32_t*>(spos + NA * 32);
   float2* sdir = reinterpret_cast<float2*>(squeue + NA * kLidarQueue);
   float2* sst = reinterpret_cast<float2*>(sdir + ((a.n_rays + 1) & ~1));
-  float* srow = reinterpret_cast<float*>(sst + (1 + NO) * 32) + i * 32 * P;
+  float* rows = reinterpret_cast<float*>(sst + (1 + NO) * 32);
+  float4* sag = reinterpret_cast<float4*>(rows);
+  float* srow = rows + i * 32 * P;
   if (threadIdx.x < a.n_rays) {
     const double dx = a.ray_dir[2 * threadIdx.x], dy = a.ray_dir[2 * threadIdx.x + 1];
     sdird[threadIdx.x] = make_double2(dx, dy);
@@ -595,10 +601,7 @@ __global__ void __launch_bounds__(32 * NA, (SS_FLOCK_WARPS / NA < 32 ? SS_FLOCK_
       if (lk.fan_ok) {
         // warp-collective: all lanes, including invalid / rotated ones
         lidar_fan_warp<NA>(fan, i, lane, NO, me.x, me.y, spos, sst, lk, sdird, wbest, P, squeue + i * kLidarQueue,
-                           a.n_rays);
-        if (fan)
-          for (int m = 0; m < a.n_rays; ++m)
-            best[m] = __float_as_uint(fminf(__uint_as_float(best[m]), range_f));
+                           a.n_rays, __float_as_uint(range_f));
       } else if (fan) {
         for (int m = 0; m < a.n_rays; ++m) best[m * stride] = 0x7f800000u;
 #pragma unroll
@@ -640,10 +643,10 @@ __global__ void __launch_bounds__(32 * NA, (SS_FLOCK_WARPS / NA < 32 ? SS_FLOCK_
 }
 
 inline size_t flocking_w_smem(int NA, int NO, int n_rays, int O) {
-  return (size_t)n_rays * sizeof(double2) + (size_t)NA * 32 * sizeof(float4) +
-         (size_t)NA * 32 * sizeof(float2) + (size_t)NA * kLidarQueue * sizeof(uint32_t) +
-         (size_t)((n_rays + 1) & ~1) * sizeof(float2) + (size_t)(1 + NO) * 32 * sizeof(float2) +
-         (size_t)NA * 32 * (O | 1) * sizeof(float);
+  const size_t rows = (size_t)NA * 32 * (O | 1) * sizeof(float), pre = (size_t)NA * 32 * sizeof(float4);
+  return (size_t)n_rays * sizeof(double2) + (size_t)NA * 32 * sizeof(float2) +
+         (size_t)NA * kLidarQueue * sizeof(uint32_t) + (size_t)((n_rays + 1) & ~1) * sizeof(float2) +
+         (size_t)(1 + NO) * 32 * sizeof(float2) + (rows > pre ? rows : pre);
 }
 
 int launch_flocking(World& w, SmallArgs& a, cudaStream_t st) {

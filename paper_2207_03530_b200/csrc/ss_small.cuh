@@ -108,18 +108,24 @@ SS_DEV void obs_bulk_drain() {
   if (kObsBulk && (threadIdx.x & 31) == 0) bulk_wait_read_all();
 }
 
-// Staging block of (warp, agent i): one per agent with SS_OBS_BULK.
+// Bulk flush when the per-agent staging blocks fit the default 48 KB of
+// dynamic shared memory (every BASELINE config does); otherwise one block per
+// warp, reused agent after agent.
+__host__ __device__ constexpr bool obs_bulk(int NA, int O) { return kObsBulk && NA * O <= 96; }
+
+// Staging block of (warp, agent i): one per agent with the bulk flush.
 SS_DEV float* obs_stage(float* smem, int i, int NA, int O) {
-  return smem + ((threadIdx.x >> 5) * (kObsBulk ? NA : 1) + (kObsBulk ? i : 0)) * (32 * O);
+  const bool bulk = obs_bulk(NA, O);
+  return smem + ((threadIdx.x >> 5) * (bulk ? NA : 1) + (bulk ? i : 0)) * (32 * O);
 }
 
-SS_DEV void obs_flush(float* __restrict__ dst, int nvalid, int O, float* __restrict__ sbuf) {
-  if (kObsBulk) warp_flush_bulk(dst, nvalid, O, sbuf);
+SS_DEV void obs_flush(float* __restrict__ dst, int nvalid, int NA, int O, float* __restrict__ sbuf) {
+  if (obs_bulk(NA, O)) warp_flush_bulk(dst, nvalid, O, sbuf);
   else warp_flush(dst, nvalid, O, sbuf);
 }
 
 inline size_t obs_stage_bytes(int NA, int O) {
-  return (size_t)kSmallThreads * O * sizeof(float) * (kObsBulk ? NA : 1);
+  return (size_t)kSmallThreads * O * sizeof(float) * (obs_bulk(NA, O) ? NA : 1);
 }
 
 // Flush staged rows whose per-lane stride P is padded to an odd number of
@@ -133,7 +139,15 @@ SS_DEV void warp_flush_padded(float* __restrict__ dst, int nvalid, int O, int P,
   // row = floor(q / O4) through a float reciprocal: (q + 0.5) / O4 sits at
   // least 0.5 / O4 from an integer and q <= 32 * O, so the float product
   // (relative error < 2^-22) always truncates to the exact quotient.
-  if ((O & 3) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
+  if ((O & 3) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0 && ((O >> 2) & ((O >> 2) - 1)) == 0) {
+    // rows of a power-of-two number of 16-byte chunks: shifts, no division
+    const int sh = __ffs(O >> 2) - 1;
+    for (int q = lane; q < (n >> 2); q += 32) {
+      const int r = q >> sh, j = (q & ((1 << sh) - 1)) << 2;
+      const float* s = sbuf + r * P + j;
+      __stcs(reinterpret_cast<float4*>(dst) + q, make_float4(s[0], s[1], s[2], s[3]));
+    }
+  } else if ((O & 3) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
     const int O4 = O >> 2;
     const float inv = 1.0f / (float)O4;
     for (int q = lane; q < (n >> 2); q += 32) {

@@ -83,15 +83,19 @@ struct SpreadEnv {
   }
 
   // simple_spread.py:48-54: [x, y, vx, vy, (marker - self), (other - self)]
+  // (8-byte shared stores: rows of 4 NA + 2 floats are 8-byte aligned, and
+  // lane offsets 4 (4 NA + 2) l hit distinct bank pairs per half warp)
   SS_DEV void obs_row(int i, float* row) const {
-    row[0] = px[i]; row[1] = py[i]; row[2] = vx[i]; row[3] = vy[i];
-    int c = 4;
+    float2* r2 = reinterpret_cast<float2*>(row);
+    r2[0] = make_float2(px[i], py[i]);
+    r2[1] = make_float2(vx[i], vy[i]);
+    int c = 2;
 #pragma unroll
-    for (int m = 0; m < NA; ++m) { row[c++] = fsub(mx[m], px[i]); row[c++] = fsub(my[m], py[i]); }
+    for (int m = 0; m < NA; ++m) r2[c++] = make_float2(fsub(mx[m], px[i]), fsub(my[m], py[i]));
 #pragma unroll
     for (int o = 0; o < NA; ++o) {
       if (o == i) continue;
-      row[c++] = fsub(px[o], px[i]); row[c++] = fsub(py[o], py[i]);
+      r2[c++] = make_float2(fsub(px[o], px[i]), fsub(py[o], py[i]));
     }
   }
 };
@@ -146,7 +150,7 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_simple_spread(
       sbuf = obs_stage(smem, i, NA, O);
       row = sbuf + (threadIdx.x & 31) * O;
       if (valid) v.obs_row(i, row);
-      if (nvalid > 0) obs_flush(a.obs + i * a.obs_stride + e0 * O, nvalid, O, sbuf);
+      if (nvalid > 0) obs_flush(a.obs + i * a.obs_stride + e0 * O, nvalid, NA, O, sbuf);
     }
     obs_bulk_drain();
   }

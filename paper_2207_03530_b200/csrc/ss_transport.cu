@@ -131,18 +131,21 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_transport(cons
       sbuf = obs_stage(smem, i, NA, O);
       row = sbuf + (threadIdx.x & 31) * O;
       if (valid) {
-        row[0] = px[i]; row[1] = py[i]; row[2] = vx[i]; row[3] = vy[i];
-        row[4] = fsub(px[NA], px[i]); row[5] = fsub(py[NA], py[i]);
         if (REV) {
+          row[0] = px[i]; row[1] = py[i]; row[2] = vx[i]; row[3] = vy[i];
+          row[4] = fsub(px[NA], px[i]); row[5] = fsub(py[NA], py[i]);
           row[6] = vx[NA]; row[7] = vy[NA];
           row[8] = fsub(gx, px[NA]); row[9] = fsub(gy, py[NA]);
         } else {
-          row[6] = fsub(gx, px[i]); row[7] = fsub(gy, py[i]);
-          row[8] = fsub(px[NA], gx); row[9] = fsub(py[NA], gy);
-          row[10] = vx[NA]; row[11] = vy[NA];
+          // 48-byte rows: three 16-byte shared stores (conflict-free per
+          // quarter warp: lane offsets 48 l span distinct bank quads)
+          float4* r4 = reinterpret_cast<float4*>(row);
+          r4[0] = make_float4(px[i], py[i], vx[i], vy[i]);
+          r4[1] = make_float4(fsub(px[NA], px[i]), fsub(py[NA], py[i]), fsub(gx, px[i]), fsub(gy, py[i]));
+          r4[2] = make_float4(fsub(px[NA], gx), fsub(py[NA], gy), vx[NA], vy[NA]);
         }
       }
-      if (nvalid > 0) obs_flush(a.obs + i * a.obs_stride + e0 * O, nvalid, O, sbuf);
+      if (nvalid > 0) obs_flush(a.obs + i * a.obs_stride + e0 * O, nvalid, NA, O, sbuf);
     }
     obs_bulk_drain();
   }
@@ -237,7 +240,7 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_dropout(const 
           row[c++] = fsub(px[o], px[i]); row[c++] = fsub(py[o], py[i]);
         }
       }
-      if (nvalid > 0) obs_flush(a.obs + i * a.obs_stride + e0 * O, nvalid, O, sbuf);
+      if (nvalid > 0) obs_flush(a.obs + i * a.obs_stride + e0 * O, nvalid, NA, O, sbuf);
     }
     obs_bulk_drain();
   }

@@ -172,10 +172,12 @@ def football(sc, i, obs):             # football.py heuristic_action
     through = _unit(to_mouth - to_ball)
     stand_off = to_ball - through * 0.09
     if i % 2 == 1:   # float64: np.array([0.0, 0.3]) promotes
-        off = torch.tensor([0.0, 0.3], dtype=F64, device=obs.device)
+        off = torch.zeros_like(stand_off, dtype=F64)
+        off[:, 1] = 0.3
         return _clip_unit(5.0 * (stand_off.to(F64) + off) + (through * 0.3).to(F64))
-    one, fifth = (torch.tensor(v, dtype=F64, device=obs.device) for v in (1.0, 0.2))
-    lean = torch.where(_norm(stand_off)[:, None] < 0.12, one, fifth)    # float64 (np.where of Python floats)
+    near = _norm(stand_off)[:, None] < 0.12
+    lean = torch.where(near, torch.full(near.shape, 1.0, dtype=F64, device=obs.device),
+                       torch.full(near.shape, 0.2, dtype=F64, device=obs.device))   # float64 (np.where of Python floats)
     return _clip_unit((5.0 * stand_off).to(F64) + through.to(F64) * lean)
 
 

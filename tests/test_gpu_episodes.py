@@ -38,8 +38,10 @@ def test_ten_seed_returns_match_reference(cuda, name):
                                 S.RandomPolicy(seed=1000 + s))[0]) for s in range(10)]
     assert heur == GOLDEN[name]["scripted"]
     assert rand == GOLDEN[name]["random"]
-    assert abs(np.mean(heur) - DOC[name][0]) <= 0.005 + 1e-9
-    assert abs(np.mean(rand) - DOC[name][1]) <= 0.005 + 1e-9
+    # the doc's two decimals round the acceptance log's three (test_output.txt:
+    # -32.085 -> -32.09, -36.875 -> -36.88): half a unit of each
+    assert abs(np.mean(heur) - DOC[name][0]) <= 0.0055
+    assert abs(np.mean(rand) - DOC[name][1]) <= 0.0055
     assert np.mean(heur) > np.mean(rand)
 
 
@@ -57,7 +59,8 @@ def test_device_controllers_equal_numpy_controllers(cuda, name):
             if y is None:
                 assert x is None
                 continue
-            got, want = x.cpu().numpy(), np.asarray(y, dtype=np.float32)
+            got = x.cpu().numpy()
+            want = y.cpu().numpy() if hasattr(y, "cpu") else np.asarray(y, dtype=np.float32)
             if name == "transport":
                 np.testing.assert_allclose(got, want, rtol=0, atol=2e-6)
             else:
