@@ -86,8 +86,17 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: Path | No
     obj_dir = OBJ_DIR if not defines else OBJ_DIR / "_".join(d.replace("=", "") for d in defines)
     obj_dir.mkdir(parents=True, exist_ok=True)
     srcs = sources()
+    # incremental: a translation unit is recompiled when its object is older
+    # than the source, any header, or this build script (flags)
+    newest_dep = max(p.stat().st_mtime for p in _headers() + [Path(__file__)])
+
+    def stale(src: Path) -> bool:
+        obj = obj_dir / (src.stem + ".o")
+        return force or verbose or not obj.exists() or obj.stat().st_mtime < max(src.stat().st_mtime, newest_dep)
+
     with cf.ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
-        objs = list(ex.map(lambda s: _compile(nvcc, s, verbose, defines, obj_dir), srcs))
+        objs = list(ex.map(lambda s: _compile(nvcc, s, verbose, defines, obj_dir) if stale(s)
+                           else obj_dir / (s.stem + ".o"), srcs))
     tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart"]
     res = subprocess.run(cmd, capture_output=True, text=True)

@@ -113,10 +113,24 @@ SS_DEV void obs_bulk_drain() {
 // warp, reused agent after agent.
 __host__ __device__ constexpr bool obs_bulk(int NA, int O) { return kObsBulk && NA * O <= 96; }
 
-// Staging block of (warp, agent i): one per agent with the bulk flush.
+// Staging buffers per warp for the bulk flush: one per agent, or a ring of
+// SS_OBS_NBUF (a buffer is reused once its previous bulk store has read it).
+#ifndef SS_OBS_NBUF
+#define SS_OBS_NBUF 0     // 0: one per agent
+#endif
+__host__ __device__ constexpr int obs_nbuf(int NA, int O) {
+  return !obs_bulk(NA, O) ? 1 : (SS_OBS_NBUF > 0 && SS_OBS_NBUF < NA ? SS_OBS_NBUF : NA);
+}
+
+// Staging block of (warp, agent i).
 SS_DEV float* obs_stage(float* smem, int i, int NA, int O) {
-  const bool bulk = obs_bulk(NA, O);
-  return smem + ((threadIdx.x >> 5) * (bulk ? NA : 1) + (bulk ? i : 0)) * (32 * O);
+  const int nb = obs_nbuf(NA, O);
+  if (obs_bulk(NA, O) && nb < NA && i >= nb) {
+    // ring: the store issued nb agents ago must have read this buffer
+    if ((threadIdx.x & 31) == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(SS_OBS_NBUF > 0 ? SS_OBS_NBUF - 1 : 0) : "memory");
+    __syncwarp();
+  }
+  return smem + ((threadIdx.x >> 5) * nb + (i % nb)) * (32 * O);
 }
 
 SS_DEV void obs_flush(float* __restrict__ dst, int nvalid, int NA, int O, float* __restrict__ sbuf) {
@@ -125,7 +139,7 @@ SS_DEV void obs_flush(float* __restrict__ dst, int nvalid, int NA, int O, float*
 }
 
 inline size_t obs_stage_bytes(int NA, int O) {
-  return (size_t)kSmallThreads * O * sizeof(float) * (obs_bulk(NA, O) ? NA : 1);
+  return (size_t)kSmallThreads * O * sizeof(float) * obs_nbuf(NA, O);
 }
 
 // Flush staged rows whose per-lane stride P is padded to an odd number of
