@@ -480,10 +480,13 @@ def run_b200(args, rank, world, local) -> None:
     stream = torch.cuda.current_stream(dev)
     # Env.step as CUDA-graph replays of S consecutive validated fused steps
     # (NaN scan + guarded launch, the eager Env.step's work without its host
-    # sync), S the largest divisor of K up to 10 while S steps' outputs stay
-    # under ~4 GB: the GPU runs step after step as in a long rollout
+    # sync), S the largest divisor of K up to 10 while the S steps' outputs
+    # (distinct graph-owned buffers) stay under 32 GB of the 180 GB HBM: the
+    # GPU runs step after step as in a long rollout, each step's scan
+    # overlapping the previous step
     out_bytes = A * B * (O * 4 + 4) + B
-    S = max(s for s in range(1, 11) if K % s == 0 and s * out_bytes <= 4e9) if out_bytes <= 4e9 else 1
+    cap = 32e9
+    S = max(s for s in range(1, 11) if K % s == 0 and s * out_bytes <= cap) if out_bytes <= cap else 1
     graph = env.step_graph(acts, steps_per_replay=S, validate=True)
     R = K // S
 
