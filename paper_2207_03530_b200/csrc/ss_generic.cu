@@ -26,20 +26,26 @@ struct GenericArgs {
   int* status;   // set to 1 when an unsupported shape pair is met
 };
 
-__global__ void __launch_bounds__(32) k_generic_physics(const GenericArgs a) {
+// One thread per env, kGenericThreads per CTA; the per-entity accumulators
+// (3 E floats per thread) are the shared-memory footprint.  Two-warp CTAs
+// lift the one-warp version's cap of 32 resident CTAs (= 50 % of the SM's
+// warps) while small worlds still fit many CTAs per SM.
+constexpr int kGenericThreads = 64;
+
+__global__ void __launch_bounds__(kGenericThreads) k_generic_physics(const GenericArgs a) {
   extern __shared__ float sm[];
   grid_dep_sync();
   if (guard_tripped(a.guard, a.guard_n)) return;
   const int lane = threadIdx.x;
   const int64_t B = a.s.B;
-  const int64_t e = (int64_t)blockIdx.x * 32 + lane;
+  const int64_t e = (int64_t)blockIdx.x * kGenericThreads + lane;
   if (e >= B) return;
   if (!(a.mode & SS_DO_PHYSICS)) {
     if (a.mode & SS_DO_COUNT) a.s.step_count[e] += 1;
     return;
   }
   // action forces (dynamics.py:151-152); decode_action (env.py:97) when flagged
-  const bool ok = env_physics(a.s, a.ph, a.ents, a.pairs, a.E, a.P, a.joints, a.J, a.A, e, sm, 32, lane,
+  const bool ok = env_physics(a.s, a.ph, a.ents, a.pairs, a.E, a.P, a.joints, a.J, a.A, e, sm, kGenericThreads, lane,
                               [&](int i, float& fx, float& fy) {
     if (a.act[i] == nullptr) return false;
     const float2 u = a.act[i][e];
@@ -78,13 +84,13 @@ int launch_generic(World& w, const SsBuffers* buf, const SsStepIO* io, const uin
   a.guard_n = io->guard_count > 0 ? io->guard_count : 1;
   a.status = d_status;
   if (!(io->mode & (SS_DO_PHYSICS | SS_DO_COUNT))) return SS_OK;
-  const size_t shmem = (size_t)3 * a.E * 32 * sizeof(float);
+  const size_t shmem = (size_t)3 * a.E * kGenericThreads * sizeof(float);
   if (shmem > 200 * 1024) { set_error("world too large for the generic step kernel"); return SS_ERR_UNSUPPORTED; }
   if (shmem > 48 * 1024) {
     cudaFuncSetAttribute(k_generic_physics, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
   }
-  const unsigned grid = (unsigned)((w.d.batch + 31) / 32);
-  launch_step(k_generic_physics, dim3(grid), dim3(32), shmem, st, a);
+  const unsigned grid = (unsigned)((w.d.batch + kGenericThreads - 1) / kGenericThreads);
+  launch_step(k_generic_physics, dim3(grid), dim3(kGenericThreads), shmem, st, a);
   return cuda_status(cudaGetLastError(), "generic world_step launch");
 }
 
