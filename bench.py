@@ -47,20 +47,28 @@ L2_BYTES = 126_000_000
 
 
 # algorithmic HBM bytes per env-step: state r/w once,
-# actions read, obs/reward/done written, step_count r/w.
-def bytes_per_env_step(scenario: str, A: int, n_other: int, obs_dim: int) -> int:
+# actions read, obs/reward/done written, step_count r/w.  Split into what
+# every step moves (actions in, outputs out) and what a launch moves once
+# (state read + written, static entities, step_count): a fused rollout of S
+# steps pays the second part once per S steps.
+def step_bytes(scenario: str, A: int, n_other: int, obs_dim: int) -> tuple[int, int]:
+    io = 8 * A + 4 * A * obs_dim + 4 * A + 1
     if scenario == "simple_spread":
-        M, S = A, A                           # movable agents, static markers
-        return 8 * A + 32 * M + 8 * S + 4 * A * obs_dim + 4 * A + 1 + 16
+        return io, 32 * A + 8 * A + 16            # agents r/w, markers, step_count r/w
     if scenario == "transport":
-        return 8 * A + 32 * (A + 1) + 8 + 8 + 4 * A * obs_dim + 4 * A + 1 + 16
+        return io, 32 * (A + 1) + 8 + 8 + 16      # agents + package r/w, goal, package rot
     if scenario == "flocking":
-        return 8 * A + 32 * A + 8 * (1 + n_other) + 4 * A * obs_dim + 4 * A + 1 + 16
+        return io, 32 * A + 8 * (1 + n_other) + 16
     if scenario == "dispersion":
-        return 8 * A + 32 * A + 8 * n_other + 4 * A * obs_dim + 4 * A + 1 + 16 + 8 + 4
+        return io + 4, 32 * A + 8 * n_other + 16 + 8   # + fresh-bites aux / eaten flags
     if scenario == "discovery":
-        return 8 * A + 32 * A + 8 * n_other + 8 * n_other + 4 * A * obs_dim + 4 * A + 1 + 16 + 8
+        return io + 8 * n_other, 32 * A + 8 * n_other + 16 + 8   # + point relocations
     raise ValueError(scenario)
+
+
+def bytes_per_env_step(scenario: str, A: int, n_other: int, obs_dim: int, steps_per_launch: int = 1) -> float:
+    per_step, per_launch = step_bytes(scenario, A, n_other, obs_dim)
+    return per_step + per_launch / steps_per_launch
 
 
 # name: scenario, overrides, envs (per GPU, or global with --strong),
@@ -468,7 +476,6 @@ def run_b200(args, rank, world, local) -> None:
     A = len(env.agents)
     O = len(env.observations()[0][0])
     n_other = len(env.world.entities) - A
-    bpe = bytes_per_env_step(scen, A, n_other, O)
     K, W = args.steps, args.warmup
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
@@ -487,8 +494,11 @@ def run_b200(args, rank, world, local) -> None:
     out_bytes = A * B * (O * 4 + 4) + B
     cap = 32e9
     S = max(s for s in range(1, 11) if K % s == 0 and s * out_bytes <= cap) if out_bytes <= cap else 1
-    graph = env.step_graph(acts, steps_per_replay=S, validate=True)
+    graph = env.step_graph(acts, steps_per_replay=S, validate=True, fused_rollout=False if args.per_step else None)
     R = K // S
+    # a fused rollout kernel moves the state once per S steps
+    bpe = bytes_per_env_step(scen, A, n_other, O, S if graph.fused_rollout else 1)
+    launches_per_replay = graph.launches_per_replay
 
     # ---- kernel-path throughput (device-resident inputs) -------------------
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(R)]
@@ -521,7 +531,7 @@ def run_b200(args, rank, world, local) -> None:
 
     # the fused step kernel alone (its share of the validated step): the same
     # replays without the NaN scan, CUDA events around each
-    kgraph = env.step_graph(acts, steps_per_replay=S)
+    kgraph = env.step_graph(acts, steps_per_replay=S, fused_rollout=False if args.per_step else None)
     for t in range(-(-W // S)):
         kgraph.step(t % pool)
     kst = [torch.cuda.Event(enable_timing=True) for _ in range(R)]
@@ -534,6 +544,7 @@ def run_b200(args, rank, world, local) -> None:
     torch.cuda.synchronize(dev)
     ms_launch = float(np.median(sorted(s.elapsed_time(e) / S for s, e in zip(kst, ken))))
     achieved = bpe * B / (ms_launch / 1e3) / 1e9
+    graph_fused = graph.fused_rollout
     del graph, kgraph
 
     # ---- end to end through the public API with host buffers --------------
@@ -582,13 +593,20 @@ def run_b200(args, rank, world, local) -> None:
                        "l2": ("working set > L2 (no flush needed)" if bpe * B > L2_BYTES else
                               f"L2-resident step: {pool} action buffers cycled, {pool * set_bytes >> 20} MiB"),
                        "validate": True,
-                       "stepping": f"Env.step_graph(steps_per_replay={S}, validate=True): CUDA-graph replays of {S} "
-                                   f"consecutive validated fused steps (NaN scan + guarded launch), {pool} action "
-                                   f"buffer(s) cycled; e2e: eager Env.step(validate=True) with host buffers"},
+                       "stepping": (f"Env.step_graph(steps_per_replay={S}, validate=True): CUDA-graph replays of "
+                                    + (f"the {S} action scans + ONE fused rollout kernel of {S} steps (state on "
+                                       "chip between them)" if graph_fused else
+                                       f"{S} consecutive validated fused steps (NaN scan + guarded launch)")
+                                    + f", {pool} action buffer(s) cycled; e2e: eager Env.step(validate=True) with "
+                                      "host buffers")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
                          "traffic_source": tsrc and f"{tsrc} (ncu --set full, one launch at {B} envs)",
-                         "bytes_per_env_step": bpe, "kernel_ms": ms_launch, "step_ms": ms_step,
+                         "bytes_per_env_step": bpe,
+                         "bytes_model": (f"per step {step_bytes(scen, A, n_other, O)[0]} B (actions, outputs) + "
+                                         f"{step_bytes(scen, A, n_other, O)[1]} B (state r/w, static, step_count) "
+                                         f"per launch of {S if graph_fused else 1} step(s)"),
+                         "kernel_ms": ms_launch, "step_ms": ms_step,
                          "kernel_share_of_step": ms_launch / ms_step, "peak_source": pk["source"]},
             "e2e": {"value": e2e_value, "unit": "agent-steps/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
@@ -599,7 +617,9 @@ def run_b200(args, rank, world, local) -> None:
                     "d2h_frac_of_pinned": d2h * E2E_K / e2e_sec / 1e9 / link["d2h"],
                     "obs_on_device": {"value": Bg * A * E2E_K / metric_sec, "h2d_bytes_per_step": h2d,
                                       "d2h_bytes_per_step": A * B * 4 + B}},
-            "gpu_launches": 2 * K,    # per step: k_check_actions + the fused step kernel
+            # per replay: the S action scans + the S step kernels or one rollout kernel
+            "gpu_launches": R * launches_per_replay,
+            "fused_rollout": graph_fused,
             "steps_per_replay": S,
             "episode_stats": {"mean_return_1step": episode["mean_return"], "envs": episode["envs"],
                               "reduced_over_ranks": world},
@@ -637,6 +657,8 @@ def main() -> None:
     ap.add_argument("--strong", action="store_true",
                     help="strong scaling: --envs / the workload's batch is the global batch, sharded over ranks")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--per-step", action="store_true",
+                    help="per-step graph replays even where a fused rollout kernel exists (A/B)")
     ap.add_argument("--soak", type=float, default=1.5, help="seconds of untimed steps for clock sampling")
     ap.add_argument("--dry-run", action="store_true", help="launch path only (no GPU work)")
     args = ap.parse_args()

@@ -221,6 +221,29 @@ typedef struct SsStepIO {
   int32_t guard_count;    /* words at guard (0 means 1) */
 } SsStepIO;
 
+/* An open-loop rollout of n_steps consecutive Env.steps in ONE launch
+ * (extension): the step kernels' work with each env's state kept on chip
+ * between the steps — it is read once before the first and written once
+ * after the last, so a step moves only its actions and outputs.  Results are
+ * bitwise those of n_steps ss_env_step calls (SS_MODE_STEP).  Scenarios
+ * without a rollout kernel return SS_ERR_UNSUPPORTED (take the per-step
+ * path).  guard (device, may be NULL): n_steps NaN words; step s runs only
+ * while words 0..s are all zero, so a NaN in step k's actions leaves the
+ * state as after step k-1.  check_actions (guard required): the call itself
+ * zeroes guard and fills guard[s] with the NaN verdict of step s's actions
+ * (env.py:85) in ONE scan launch over all the steps, before the rollout. */
+#define SS_MAX_ROLLOUT 16
+typedef struct SsRolloutIO {
+  int32_t n_steps;                 /* 1 .. SS_MAX_ROLLOUT */
+  const float* const* actions;     /* HOST [n_steps * n_agents] device pointers, each [B][2] f32 */
+  float* const* obs;               /* HOST [n_steps] device pointers, layout of SsStepIO.obs */
+  int64_t obs_agent_stride;
+  float* const* rew;               /* HOST [n_steps] device pointers, each [n_agents][B] */
+  uint8_t* const* done;            /* HOST [n_steps] device pointers, each [B] */
+  int32_t* guard;                  /* device [n_steps] or NULL */
+  int32_t check_actions;           /* nonzero: scan the actions into guard first */
+} SsRolloutIO;
+
 typedef struct SsLidarDesc {
   int32_t n_rays;
   double max_range;       /* compared/returned as in sensors.py:135 */
@@ -241,6 +264,11 @@ int ss_world_destroy(void* world);
  * SS_SCN_PHYSICS_ONLY only SS_DO_PHYSICS|SS_DO_COUNT apply (world_step,
  * dynamics.py:123-184). */
 int ss_env_step(void* world, const SsBuffers* buf, const SsStepIO* io, void* stream);
+
+/* n_steps fused steps in one launch (SsRolloutIO): simple_spread and
+ * transport / reverse_transport without sub-steps; SS_ERR_UNSUPPORTED
+ * otherwise. */
+int ss_env_rollout(void* world, const SsBuffers* buf, const SsRolloutIO* io, void* stream);
 
 /* Env.reset (env.py:189-198) -> Scenario.reset_world_at.  mask == NULL
  * resets every env with the reference's whole-batch draw order (x block then

@@ -23,6 +23,7 @@ int main(void) {
   Z(SsBuffers); F(SsBuffers, rng); F(SsBuffers, rng_cur);
   Z(SsStepIO); F(SsStepIO, obs_agent_stride); F(SsStepIO, mode); F(SsStepIO, guard); F(SsStepIO, raw_forces);
   F(SsStepIO, guard_count);
+  Z(SsRolloutIO); F(SsRolloutIO, actions); F(SsRolloutIO, obs_agent_stride); F(SsRolloutIO, guard); F(SsRolloutIO, check_actions);
   Z(SsLidarDesc); F(SsLidarDesc, max_range); F(SsLidarDesc, dir_table);
   printf("\"end\": 0}\n");
   return 0;

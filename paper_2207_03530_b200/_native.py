@@ -88,6 +88,15 @@ class SsStepIO(ctypes.Structure):
                 ("raw_forces", c_i32), ("guard_count", c_i32)]
 
 
+MAX_ROLLOUT = 16
+
+
+class SsRolloutIO(ctypes.Structure):
+    _fields_ = [("n_steps", c_i32), ("actions", ctypes.POINTER(c_vp)), ("obs", ctypes.POINTER(c_vp)),
+                ("obs_agent_stride", c_i64), ("rew", ctypes.POINTER(c_vp)), ("done", ctypes.POINTER(c_vp)),
+                ("guard", c_vp), ("check_actions", c_i32)]
+
+
 class SsLidarDesc(ctypes.Structure):
     _fields_ = [("n_rays", c_i32), ("max_range", c_f64), ("start_angle", c_f64), ("span", c_f64),
                 ("attach_rotation", c_i32), ("dir_table", c_vp)]
@@ -103,6 +112,7 @@ def _declare(lib) -> None:
     lib.ss_world_create.argtypes = [P(SsWorldDesc), P(c_vp)]
     lib.ss_world_destroy.argtypes = [c_vp]
     lib.ss_env_step.argtypes = [c_vp, P(SsBuffers), P(SsStepIO), c_vp]
+    lib.ss_env_rollout.argtypes = [c_vp, P(SsBuffers), P(SsRolloutIO), c_vp]
     lib.ss_world_step.argtypes = [c_vp, P(SsBuffers), P(c_vp), P(ctypes.c_uint64), c_i32, c_vp, c_i32, c_vp, c_vp]
     lib.ss_reset.argtypes = [c_vp, P(SsBuffers), c_vp, c_vp, c_vp, c_vp]
     lib.ss_mask_count.argtypes = [c_vp, c_vp, c_vp, c_vp]
@@ -114,7 +124,7 @@ def _declare(lib) -> None:
                                        c_vp, c_vp, c_vp, c_i64, c_vp]
     lib.ss_closest_points.argtypes = [c_vp, c_vp, c_i32, c_f64, c_f64, c_vp, c_vp, c_i32,
                                       c_f64, c_f64, c_vp, c_vp, c_i64, c_vp, c_vp]
-    for name in ("ss_world_create", "ss_world_destroy", "ss_env_step", "ss_world_step", "ss_reset",
+    for name in ("ss_world_create", "ss_world_destroy", "ss_env_step", "ss_env_rollout", "ss_world_step", "ss_reset",
                  "ss_mask_count", "ss_check_actions", "ss_lidar", "ss_cast_ray", "ss_collision_force",
                  "ss_closest_points", "ss_np_trig"):
         getattr(lib, name).restype = c_i32
@@ -139,7 +149,7 @@ def lib():
 
 def exported_symbols() -> list[str]:
     return [
-        "ss_abi_version", "ss_last_error", "ss_world_create", "ss_world_destroy", "ss_env_step",
+        "ss_abi_version", "ss_last_error", "ss_world_create", "ss_world_destroy", "ss_env_step", "ss_env_rollout",
         "ss_world_step", "ss_reset", "ss_mask_count", "ss_check_actions", "ss_lidar",
         "ss_cast_ray", "ss_collision_force", "ss_closest_points", "ss_np_trig",
     ]

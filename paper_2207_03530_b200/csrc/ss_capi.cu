@@ -24,6 +24,7 @@ int cuda_status(cudaError_t e, const char* what) {
 
 int launch_small(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_t st);
 int launch_large(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_t st);
+int launch_rollout(World& w, const SsBuffers* buf, const SsRolloutIO* io, cudaStream_t st);
 int launch_generic(World& w, const SsBuffers* buf, const SsStepIO* io, const uint64_t* decode_mask,
                    int* d_status, cudaStream_t st);
 int launch_reset(World& w, const SsBuffers* buf, const uint8_t* mask, const int64_t* mask_base,
@@ -201,6 +202,17 @@ int ss_env_step(void* world, const SsBuffers* buf, const SsStepIO* io, void* str
     default:
       return launch_generic(*w, buf, io, nullptr, nullptr, st);
   }
+}
+
+int ss_env_rollout(void* world, const SsBuffers* buf, const SsRolloutIO* io, void* stream) {
+  World* w = static_cast<World*>(world);
+  if (!w || !buf || !io) { set_error("null argument"); return SS_ERR_CONTRACT; }
+  if (io->n_steps < 1 || io->n_steps > SS_MAX_ROLLOUT || !io->actions || !io->obs || !io->rew || !io->done) {
+    set_error("rollout: 1.." + std::to_string(SS_MAX_ROLLOUT) + " steps with actions and outputs per step");
+    return SS_ERR_CONTRACT;
+  }
+  if (io->check_actions && !io->guard) { set_error("rollout: check_actions needs guard words"); return SS_ERR_CONTRACT; }
+  return launch_rollout(*w, buf, io, static_cast<cudaStream_t>(stream));
 }
 
 int ss_world_step(void* world, const SsBuffers* buf, const float* const* forces,

@@ -166,7 +166,15 @@ __global__ void __launch_bounds__(512) k_check_actions(const CheckArgs a) {
     for (int i = 0; i < a.A; ++i) {
       const float4* p = reinterpret_cast<const float4*>(a.act[i]);
       if (p == nullptr) continue;           // a script drives this agent (no raw action)
-      for (int64_t k = t0; k < n4; k += stride) {
+      int64_t k = t0;
+      for (; k + 3 * stride < n4; k += 4 * stride) {   // four 16-byte loads in flight
+        float4 v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = __ldcs(p + k + j * stride);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bad |= isnan(v[j].x) | isnan(v[j].y) | isnan(v[j].z) | isnan(v[j].w);
+      }
+      for (; k < n4; k += stride) {
         const float4 v = __ldcs(p + k);
         bad |= isnan(v.x) | isnan(v.y) | isnan(v.z) | isnan(v.w);
       }

@@ -185,6 +185,41 @@ SS_DEV float decode_axis(float raw, const SsEntityDesc& d, int raw_forces) {
   return raw_forces ? raw : fmul(clip_sym(raw, d.u_range), d.u_mult);
 }
 
+// Rollout kernels: resident CTAs per SM the register budget is sized for,
+// and whether step s+1's actions are loaded before step s computes.
+#ifndef SS_ROLLOUT_MINB
+#define SS_ROLLOUT_MINB 5   // 5 x 128 threads: <= 96 registers (tools/sweep_variants.py, SWEEP_S=10)
+#endif
+#ifndef SS_ROLLOUT_PREFETCH
+#define SS_ROLLOUT_PREFETCH 1
+#endif
+
+// Per-step pointers of a fused rollout (SsRolloutIO): the step kernels'
+// SmallArgs plus, for each of n_steps steps, its actions and outputs.
+struct RolloutArgs {
+  SmallArgs a;
+  int n_steps;
+  const float2* act[SS_MAX_ROLLOUT][kSmallMaxAgents];
+  float* obs[SS_MAX_ROLLOUT];
+  float* rew[SS_MAX_ROLLOUT];
+  uint8_t* done[SS_MAX_ROLLOUT];
+  const int* guard;   // [n_steps] or nullptr
+};
+
+// Step s of a rollout runs iff its NaN words 0..s are all zero (sticky).
+// Steps a rollout launch runs: up to (excluding) the first step whose scan
+// (or an earlier one) found a NaN.  The scans completed before the launch
+// (grid_dep_sync), so one read of the S words at entry decides it.
+SS_DEV int rollout_len(const int* g, int n) {
+  if (g == nullptr) return n;
+  for (int s = 0; s < n; ++s)
+    if (g[s]) return s;
+  return n;
+}
+
+int launch_spread_rollout(World& w, RolloutArgs& r, cudaStream_t st);
+int launch_transport_rollout(World& w, RolloutArgs& r, cudaStream_t st);
+
 // Host launchers, one per translation unit (a: filled by launch_small; grid /
 // shmem derived from it).  Each returns an SsStatus.
 int launch_spread(World& w, SmallArgs& a, cudaStream_t st);

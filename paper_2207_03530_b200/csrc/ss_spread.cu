@@ -157,6 +157,93 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_simple_spread(
 }
 
 // ---------------------------------------------------------------------------
+// simple_spread, fused open-loop rollout (SsRolloutIO): the step kernel's
+// arithmetic for n_steps consecutive steps with the env's agents (and its
+// static markers) held in registers between them — state is read once and
+// written once per launch, each step moves only its actions and outputs.
+// ---------------------------------------------------------------------------
+template <int NA>
+__global__ void __launch_bounds__(kSmallThreads, SS_ROLLOUT_MINB) k_simple_spread_rollout(const RolloutArgs r) {
+  extern __shared__ __align__(16) float smem[];
+  grid_dep_sync();
+  const SmallArgs& a = r.a;
+  constexpr int O = SpreadEnv<NA>::O;
+  const int64_t B = a.s.B;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = e < B;
+  const int64_t e0 = e - (threadIdx.x & 31);
+  const int nvalid = (int)min((int64_t)32, B - e0);
+  SpreadEnv<NA> v;
+  int64_t steps = 0;
+  if (valid) {
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      const float4 q = a.s.dyn[i * B + e];
+      v.px[i] = q.x; v.py[i] = q.y; v.vx[i] = q.z; v.vy[i] = q.w;
+      const float2 m = a.s.stat[i * B + e];
+      v.mx[i] = m.x; v.my[i] = m.y;
+    }
+    steps = a.s.step_count[e];
+  }
+  const int n_run = rollout_len(r.guard, r.n_steps);   // uniform over the grid
+  float2 u[NA];
+  if (valid && n_run > 0) {
+#pragma unroll
+    for (int i = 0; i < NA; ++i) u[i] = __ldcs(r.act[0][i] + e);
+  }
+  for (int s = 0; s < n_run; ++s) {
+    float2 un[NA];   // the next step's actions, in flight during this step
+    if (SS_ROLLOUT_PREFETCH && valid && s + 1 < n_run) {
+#pragma unroll
+      for (int i = 0; i < NA; ++i) un[i] = __ldcs(r.act[s + 1][i] + e);
+    }
+    if (valid) {
+      v.template physics<false>(u, a);
+      steps += 1;
+      float rew[NA];
+      v.rewards(a, rew);
+#pragma unroll
+      for (int i = 0; i < NA; ++i) __stcs(r.rew[s] + i * B + e, rew[i]);
+      r.done[s][e] = (uint8_t)(steps >= a.ph.max_steps);
+    }
+    if (s > 0) {   // the previous step's bulk stores must have read the staging
+      obs_bulk_drain();
+      __syncwarp();
+    }
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      float* sbuf = obs_stage(smem, i, NA, O);
+      float* row = sbuf + (threadIdx.x & 31) * O;
+      if (valid) v.obs_row(i, row);
+      if (nvalid > 0) obs_flush(r.obs[s] + i * a.obs_stride + e0 * O, nvalid, NA, O, sbuf);
+    }
+    if (SS_ROLLOUT_PREFETCH) {
+#pragma unroll
+      for (int i = 0; i < NA; ++i) u[i] = un[i];
+    } else if (valid && s + 1 < n_run) {
+#pragma unroll
+      for (int i = 0; i < NA; ++i) u[i] = __ldcs(r.act[s + 1][i] + e);
+    }
+  }
+  if (valid) {
+#pragma unroll
+    for (int i = 0; i < NA; ++i) a.s.dyn[i * B + e] = make_float4(v.px[i], v.py[i], v.vx[i], v.vy[i]);
+    a.s.step_count[e] = steps;
+  }
+  obs_bulk_drain();
+}
+
+int launch_spread_rollout(World& w, RolloutArgs& r, cudaStream_t st) {
+  const int NA = w.d.n_agents;
+  const unsigned grid = (unsigned)((w.d.batch + kSmallThreads - 1) / kSmallThreads);
+  const size_t shmem = obs_stage_bytes(NA, w.d.obs_dim);
+#define SS_CASE(n) case n: launch_step(k_simple_spread_rollout<n>, dim3(grid), dim3(kSmallThreads), shmem, st, r); break;
+  switch (NA) { SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) }
+#undef SS_CASE
+  return cuda_status(cudaGetLastError(), "simple_spread rollout launch");
+}
+
+// ---------------------------------------------------------------------------
 // simple_spread, persistent bulk-copy pipeline (full Env.step mode only).
 // Each CTA walks tiles of 128 consecutive envs; the next tile's inputs
 // (agent rows, marker rows, actions, step_count — all contiguous spans) are

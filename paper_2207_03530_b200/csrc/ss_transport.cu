@@ -15,6 +15,83 @@ namespace ss {
 // REV = 1: reverse_transport (catalog scenarios/reverse_transport.py): the
 // same world (agents inside a hollow crate), observation
 // [x, y, vx, vy, crate - self, crate vel, goal - crate] (O = 10).
+// One physics (sub-)step of transport for env e: forces from `act` (decoded
+// actions + gravity), contacts in the reference's pair order (agent pairs,
+// then agent i vs the package box), integrate; STORE: write each state row
+// as soon as it is final.
+template <int NA, bool STORE>
+SS_DEV void transport_physics(float (&px)[NA + 1], float (&py)[NA + 1], float (&vx)[NA + 1],
+                              float (&vy)[NA + 1], const float2 (&act)[NA], float ca, float sa,
+                              const SmallArgs& a, int64_t B, int64_t e) {
+  const double hx = a.sd[0], hy = a.sd[1];
+  float fx[NA + 1], fy[NA + 1];
+#pragma unroll
+  for (int i = 0; i < NA; ++i) {
+    const SsEntityDesc& d = a.ents[i];
+    fx[i] = decode_axis(act[i].x, d, a.raw_forces);
+    fy[i] = decode_axis(act[i].y, d, a.raw_forces);
+  }
+  fx[NA] = 0.0f; fy[NA] = 0.0f;
+  if (a.ph.has_gravity) {
+#pragma unroll
+    for (int i = 0; i <= NA; ++i) {
+      fx[i] = fadd(fx[i], a.ents[i].grav_x); fy[i] = fadd(fy[i], a.ents[i].grav_y);
+    }
+  }
+  int p = 0;
+#pragma unroll
+  for (int i = 0; i < NA; ++i) {
+#pragma unroll
+    for (int j = i + 1; j < NA; ++j, ++p) {
+      const SsPairDesc pr = a.pairs[p];
+      float cx, cy;
+      if (contact_force(px[i], py[i], px[j], py[j], pr.d_min, pr.d2_act, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
+        fx[i] = fadd(fx[i], cx); fy[i] = fadd(fy[i], cy);
+        fx[j] = fsub(fx[j], cx); fy[j] = fsub(fy[j], cy);
+      }
+    }
+    {  // agent i vs package (sphere-box)
+      const SsPairDesc pr = a.pairs[p++];
+      float qx, qy, cx, cy;
+      closest_point_on_box(px[i], py[i], px[NA], py[NA], ca, sa, hx, hy, qx, qy);
+      if (contact_force(px[i], py[i], qx, qy, pr.d_min, pr.d2_act, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
+        fx[i] = fadd(fx[i], cx); fy[i] = fadd(fy[i], cy);
+        fx[NA] = fsub(fx[NA], cx); fy[NA] = fsub(fy[NA], cy);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i <= NA; ++i) {
+    const SsEntityDesc& d = a.ents[i];
+    integrate_lin(px[i], py[i], vx[i], vy[i], fx[i], fy[i], a.ph.keep, d.inv_m_dt, a.ph.dt,
+                  d.max_speed);
+    // single step: store each row as soon as it is final (the LSU drains
+    // the stores while the next entity integrates)
+    if (STORE) a.s.dyn[i * B + e] = make_float4(px[i], py[i], vx[i], vy[i]);
+  }
+}
+
+// Observation row of agent i: [x, y, vx, vy, package - self, goal - self,
+// package - goal, package vel] (REV: [x, y, vx, vy, crate - self, crate vel,
+// goal - crate]).
+template <int NA, int REV>
+SS_DEV void transport_obs_row(int i, float* row, const float (&px)[NA + 1], const float (&py)[NA + 1],
+                              const float (&vx)[NA + 1], const float (&vy)[NA + 1], float gx, float gy) {
+  if (REV) {
+    row[0] = px[i]; row[1] = py[i]; row[2] = vx[i]; row[3] = vy[i];
+    row[4] = fsub(px[NA], px[i]); row[5] = fsub(py[NA], py[i]);
+    row[6] = vx[NA]; row[7] = vy[NA];
+    row[8] = fsub(gx, px[NA]); row[9] = fsub(gy, py[NA]);
+  } else {
+    // 48-byte rows: three 16-byte shared stores (conflict-free per
+    // quarter warp: lane offsets 48 l span distinct bank quads)
+    float4* r4 = reinterpret_cast<float4*>(row);
+    r4[0] = make_float4(px[i], py[i], vx[i], vy[i]);
+    r4[1] = make_float4(fsub(px[NA], px[i]), fsub(py[NA], py[i]), fsub(gx, px[i]), fsub(gy, py[i]));
+    r4[2] = make_float4(fsub(px[NA], gx), fsub(py[NA], gy), vx[NA], vy[NA]);
+  }
+}
+
 template <int NA, int REV, bool MS>
 __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_transport(const SmallArgs a) {
   extern __shared__ __align__(16) float smem[];
@@ -47,57 +124,7 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_transport(cons
   if (valid && (a.mode & SS_DO_PHYSICS)) {
     float ca, sa;
     if (prot == 0.0f) { ca = 1.0f; sa = prot; } else { ca = np_cosf(prot); sa = np_sinf(prot); }
-    const double hx = a.sd[0], hy = a.sd[1];
-    // one physics sub-step: forces from `act` (decoded actions + gravity),
-    // contacts in pair order, integrate
-    auto substep = [&](const float2 (&act)[NA]) {
-      float fx[NA + 1], fy[NA + 1];
-#pragma unroll
-      for (int i = 0; i < NA; ++i) {
-        const SsEntityDesc& d = a.ents[i];
-        fx[i] = decode_axis(act[i].x, d, a.raw_forces);
-        fy[i] = decode_axis(act[i].y, d, a.raw_forces);
-      }
-      fx[NA] = 0.0f; fy[NA] = 0.0f;
-      if (a.ph.has_gravity) {
-#pragma unroll
-        for (int i = 0; i <= NA; ++i) {
-          fx[i] = fadd(fx[i], a.ents[i].grav_x); fy[i] = fadd(fy[i], a.ents[i].grav_y);
-        }
-      }
-      int p = 0;
-#pragma unroll
-      for (int i = 0; i < NA; ++i) {
-#pragma unroll
-        for (int j = i + 1; j < NA; ++j, ++p) {
-          const SsPairDesc pr = a.pairs[p];
-          float cx, cy;
-          if (contact_force(px[i], py[i], px[j], py[j], pr.d_min, pr.d2_act, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
-            fx[i] = fadd(fx[i], cx); fy[i] = fadd(fy[i], cy);
-            fx[j] = fsub(fx[j], cx); fy[j] = fsub(fy[j], cy);
-          }
-        }
-        {  // agent i vs package (sphere-box)
-          const SsPairDesc pr = a.pairs[p++];
-          float qx, qy, cx, cy;
-          closest_point_on_box(px[i], py[i], px[NA], py[NA], ca, sa, hx, hy, qx, qy);
-          if (contact_force(px[i], py[i], qx, qy, pr.d_min, pr.d2_act, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
-            fx[i] = fadd(fx[i], cx); fy[i] = fadd(fy[i], cy);
-            fx[NA] = fsub(fx[NA], cx); fy[NA] = fsub(fy[NA], cy);
-          }
-        }
-      }
-#pragma unroll
-      for (int i = 0; i <= NA; ++i) {
-        const SsEntityDesc& d = a.ents[i];
-        integrate_lin(px[i], py[i], vx[i], vy[i], fx[i], fy[i], a.ph.keep, d.inv_m_dt, a.ph.dt,
-                      d.max_speed);
-        // single step: store each row as soon as it is final (the LSU drains
-        // the stores while the next entity integrates)
-        if (!MS) a.s.dyn[i * B + e] = make_float4(px[i], py[i], vx[i], vy[i]);
-      }
-    };
-    substep(u);
+    transport_physics<NA, !MS>(px, py, vx, vy, u, ca, sa, a, B, e);
     // further physics sub-steps (PhysK.substeps > 1: the MS instantiation,
     // so the reference's single step keeps its register budget) reload the
     // held actions instead of keeping them live across the first one
@@ -105,7 +132,7 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_transport(cons
       float2 ur[NA];
 #pragma unroll
       for (int i = 0; i < NA; ++i) ur[i] = a.act[i][e];
-      substep(ur);
+      transport_physics<NA, false>(px, py, vx, vy, ur, ca, sa, a, B, e);
     }
     if (MS) {
 #pragma unroll
@@ -130,25 +157,88 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_transport(cons
     for (int i = 0; i < NA; ++i) {
       sbuf = obs_stage(smem, i, NA, O);
       row = sbuf + (threadIdx.x & 31) * O;
-      if (valid) {
-        if (REV) {
-          row[0] = px[i]; row[1] = py[i]; row[2] = vx[i]; row[3] = vy[i];
-          row[4] = fsub(px[NA], px[i]); row[5] = fsub(py[NA], py[i]);
-          row[6] = vx[NA]; row[7] = vy[NA];
-          row[8] = fsub(gx, px[NA]); row[9] = fsub(gy, py[NA]);
-        } else {
-          // 48-byte rows: three 16-byte shared stores (conflict-free per
-          // quarter warp: lane offsets 48 l span distinct bank quads)
-          float4* r4 = reinterpret_cast<float4*>(row);
-          r4[0] = make_float4(px[i], py[i], vx[i], vy[i]);
-          r4[1] = make_float4(fsub(px[NA], px[i]), fsub(py[NA], py[i]), fsub(gx, px[i]), fsub(gy, py[i]));
-          r4[2] = make_float4(fsub(px[NA], gx), fsub(py[NA], gy), vx[NA], vy[NA]);
-        }
-      }
+      if (valid) transport_obs_row<NA, REV>(i, row, px, py, vx, vy, gx, gy);
       if (nvalid > 0) obs_flush(a.obs + i * a.obs_stride + e0 * O, nvalid, NA, O, sbuf);
     }
     obs_bulk_drain();
   }
+}
+
+// transport, fused open-loop rollout (SsRolloutIO): n_steps steps with the
+// agents and the package in registers between them (the goal and the
+// package's fixed rotation read once); state read once, written once.
+template <int NA, int REV>
+__global__ void __launch_bounds__(kSmallThreads, SS_ROLLOUT_MINB) k_transport_rollout(const RolloutArgs r) {
+  extern __shared__ __align__(16) float smem[];
+  grid_dep_sync();
+  const SmallArgs& a = r.a;
+  constexpr int O = REV ? 10 : 12;
+  const int64_t B = a.s.B;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = e < B;
+  const int64_t e0 = e - (threadIdx.x & 31);
+  const int nvalid = (int)min((int64_t)32, B - e0);
+  float px[NA + 1], py[NA + 1], vx[NA + 1], vy[NA + 1];
+  float gx = 0.f, gy = 0.f, prot = 0.f;
+  int64_t steps = 0;
+  if (valid) {
+#pragma unroll
+    for (int i = 0; i <= NA; ++i) {
+      const float4 q = a.s.dyn[i * B + e];
+      px[i] = q.x; py[i] = q.y; vx[i] = q.z; vy[i] = q.w;
+    }
+    const float2 g = a.s.stat[e];
+    gx = g.x; gy = g.y;
+    prot = a.s.rot[NA * B + e].x;
+    steps = a.s.step_count[e];
+  }
+  float ca, sa;
+  if (prot == 0.0f) { ca = 1.0f; sa = prot; } else { ca = np_cosf(prot); sa = np_sinf(prot); }
+  const int n_run = rollout_len(r.guard, r.n_steps);   // uniform over the grid
+  float2 u[NA];
+  if (valid && n_run > 0) {
+#pragma unroll
+    for (int i = 0; i < NA; ++i) u[i] = __ldcs(r.act[0][i] + e);
+  }
+  for (int s = 0; s < n_run; ++s) {
+    float2 un[NA];   // the next step's actions, in flight during this step
+    if (SS_ROLLOUT_PREFETCH && valid && s + 1 < n_run) {
+#pragma unroll
+      for (int i = 0; i < NA; ++i) un[i] = __ldcs(r.act[s + 1][i] + e);
+    }
+    if (valid) {
+      transport_physics<NA, false>(px, py, vx, vy, u, ca, sa, a, B, e);
+      steps += 1;
+      const float gap = norm2(fsub(px[NA], gx), fsub(py[NA], gy));
+#pragma unroll
+      for (int i = 0; i < NA; ++i) __stcs(r.rew[s] + i * B + e, -gap);
+      r.done[s][e] = (uint8_t)((gap < a.sc[2]) | (steps >= a.ph.max_steps));
+    }
+    if (s > 0) {   // the previous step's bulk stores must have read the staging
+      obs_bulk_drain();
+      __syncwarp();
+    }
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      float* sbuf = obs_stage(smem, i, NA, O);
+      float* row = sbuf + (threadIdx.x & 31) * O;
+      if (valid) transport_obs_row<NA, REV>(i, row, px, py, vx, vy, gx, gy);
+      if (nvalid > 0) obs_flush(r.obs[s] + i * a.obs_stride + e0 * O, nvalid, NA, O, sbuf);
+    }
+    if (SS_ROLLOUT_PREFETCH) {
+#pragma unroll
+      for (int i = 0; i < NA; ++i) u[i] = un[i];
+    } else if (valid && s + 1 < n_run) {
+#pragma unroll
+      for (int i = 0; i < NA; ++i) u[i] = __ldcs(r.act[s + 1][i] + e);
+    }
+  }
+  if (valid) {
+#pragma unroll
+    for (int i = 0; i <= NA; ++i) a.s.dyn[i * B + e] = make_float4(px[i], py[i], vx[i], vy[i]);
+    a.s.step_count[e] = steps;
+  }
+  obs_bulk_drain();
 }
 
 // ---------------------------------------------------------------------------
@@ -264,6 +354,20 @@ int launch_transport(World& w, SmallArgs& a, cudaStream_t st) {
   switch (NA) { SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) }
 #undef SS_CASE
   return cuda_status(cudaGetLastError(), "transport step launch");
+}
+
+int launch_transport_rollout(World& w, RolloutArgs& r, cudaStream_t st) {
+  const int NA = w.d.n_agents;
+  const unsigned grid = (unsigned)((w.d.batch + kSmallThreads - 1) / kSmallThreads);
+  const size_t shmem = obs_stage_bytes(NA, w.d.obs_dim);
+#define SS_CASE(n)                                                                                   \
+  case n:                                                                                            \
+    if (w.d.si[1]) launch_step(k_transport_rollout<n, 1>, dim3(grid), dim3(kSmallThreads), shmem, st, r); \
+    else launch_step(k_transport_rollout<n, 0>, dim3(grid), dim3(kSmallThreads), shmem, st, r);           \
+    break;
+  switch (NA) { SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) }
+#undef SS_CASE
+  return cuda_status(cudaGetLastError(), "transport rollout launch");
 }
 
 int launch_dropout(World& w, SmallArgs& a, cudaStream_t st) {

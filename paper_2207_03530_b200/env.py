@@ -397,13 +397,18 @@ class Env:
         finally:
             self.validate = saved
 
-    def step_graph(self, actions, steps_per_replay: int = 1, validate: bool = False) -> "StepGraph":
+    def step_graph(self, actions, steps_per_replay: int = 1, validate: bool = False,
+                   fused_rollout: bool | None = None) -> "StepGraph":
         """Capture Env.step into CUDA graphs over the given action buffer(s).
 
         validate=True keeps the reference's NaN check inside the graph: each
         step scans its actions and is a no-op once any NaN was seen in the
-        replay; StepGraph.check() raises ContractViolation afterwards."""
-        return StepGraph(self, actions, steps_per_replay, validate)
+        replay; StepGraph.check() raises ContractViolation afterwards.
+        fused_rollout: the S steps of a replay as ONE launch with the state
+        kept on chip between them (bitwise the same results) — None: where
+        the scenario prefers it (simple_spread), True: wherever a rollout
+        kernel exists (simple_spread, transport), False: never."""
+        return StepGraph(self, actions, steps_per_replay, validate, fused_rollout)
 
     @property
     def _any_obs_noise(self) -> bool:
@@ -448,7 +453,12 @@ class StepGraph:
     (discovery) get one graph per half of the double-buffered Philox state.
     """
 
-    def __init__(self, env: Env, actions, steps_per_replay: int = 1, validate: bool = False):
+    @staticmethod
+    def _rng_mode_of(sc) -> bool:
+        return bool(getattr(sc, "advances_rng_per_step", False))
+
+    def __init__(self, env: Env, actions, steps_per_replay: int = 1, validate: bool = False,
+                 fused_rollout: bool | None = None):
         acts = [actions] if isinstance(actions, torch.Tensor) else list(actions)
         A, B = len(env.agents), env.batch_size
         S = int(steps_per_replay)
@@ -472,6 +482,18 @@ class StepGraph:
         # NaN verdict of the replay (validate=True), zeroed at its start
         self.nan_flag = torch.zeros(S, dtype=torch.int32, device=env.device) if validate else None
         sc, world = env.scenario, env.world
+        # S > 1 steps of a world with a rollout kernel: one fused launch per
+        # replay, the state on chip between the steps (see Env.step_graph;
+        # otherwise S separate step kernels)
+        self._fused_rollout = (fused_rollout is not False and S > 1 and S <= N.MAX_ROLLOUT and not self._generic
+                               and not self._rng_mode_of(sc) and type(sc).info is _BASE_INFO
+                               and hasattr(sc, "rollout_capable") and sc.rollout_capable(world)
+                               and (fused_rollout is True or sc.rollout_preferred(world)))
+        self.fused_rollout = self._fused_rollout
+        # kernels of this library per replay: the step kernels (or the one
+        # rollout kernel) plus the action scans
+        self.launches_per_replay = ((1 + (1 if validate else 0)) if self._fused_rollout
+                                    else S + (S if validate else 0))
         self._rng_mode = bool(getattr(sc, "advances_rng_per_step", False))
         world.ensure_device_rng()
         if not env.fused:
@@ -520,6 +542,11 @@ class StepGraph:
                 g = torch.cuda.CUDAGraph()
                 results = []
                 with torch.cuda.stream(stream), torch.cuda.graph(g, stream=stream):
+                    if self._fused_rollout:
+                        results = self._capture_rollout(env, acts, i, A, B, S, stream)
+                        self._graphs[(cur, i)] = g
+                        self._results[(cur, i)] = results
+                        continue
                     scanned = self._capture_scans(env, acts, i, A, B, S, stream) if self.nan_flag is not None else None
                     for k in range(S):
                         act = acts[(i + k) % len(acts)]
@@ -535,6 +562,26 @@ class StepGraph:
                         stream.wait_stream(self._side)
                 self._graphs[(cur, i)] = g
                 self._results[(cur, i)] = results
+
+    def _capture_rollout(self, env, acts, i, A, B, S, stream) -> list:
+        """The S steps as ONE fused rollout launch (ss_env_rollout: the state
+        stays on chip between the steps), preceded, when validating, by one
+        scan launch over the S action sets (the kernel runs step k only while
+        scans 0..k found no NaN)."""
+        sc, world = env.scenario, env.world
+        ptrs = []
+        for k in range(S):
+            act = acts[(i + k) % len(acts)]
+            base, stride = act.data_ptr(), B * 8
+            ptrs.append([base + a * stride for a in range(A)])
+        outs = sc.launch_rollout(world, ptrs, guard=self.nan_flag, stream=stream.cuda_stream,
+                                 check_actions=self.nan_flag is not None)
+        res = []
+        for obs, rew, done in outs:
+            obs_list = list((obs if obs.shape[1] == B else obs[:, :B]).unbind(0))
+            res.append(StepResult(obs=obs_list, rewards=list(rew.unbind(0)), dones=done,
+                                  infos=[{} for _ in env.agents]))
+        return res
 
     def _capture_scans(self, env, acts, i, A, B, S, stream) -> list:
         """The replay's S action NaN scans (ss_check_actions) on a side branch

@@ -141,6 +141,45 @@ class FusedScenario(Scenario):
             world.rng.flip()
         return obs, rew, done
 
+    def rollout_capable(self, world: World) -> bool:
+        """A fused multi-step rollout kernel exists for this world
+        (ss_env_rollout: simple_spread, transport / reverse_transport with
+        their kernel's template, one physics step per Env.step)."""
+        return (self.native_id in (N.SCN_SIMPLE_SPREAD, N.SCN_TRANSPORT) and self.physics_fused(world)
+                and world.params.substeps == 1 and len(world.agents) <= 8)
+
+    def rollout_preferred(self, world: World) -> bool:
+        """Take the rollout kernel by default (StepGraph fused_rollout=None):
+        where the step is bound by its HBM traffic, which the rollout cuts.
+        transport's step is latency / issue bound (the box-contact physics),
+        so its rollout kernel is no faster than the per-step graph (measured,
+        DESIGN.md) and stays opt-in."""
+        return self.native_id == N.SCN_SIMPLE_SPREAD and self.rollout_capable(world)
+
+    def launch_rollout(self, world: World, step_action_ptrs: list, guard=None, stream: int | None = None,
+                       check_actions: bool = False) -> list:
+        """n = len(step_action_ptrs) consecutive full steps in ONE launch
+        (ss_env_rollout), the state kept on chip between them; returns the n
+        (obs, rew, done) output triples, bitwise those of n launch(MODE_STEP).
+        check_actions: the call scans the n action sets into guard (n int32
+        words) first, one launch; step s runs while words 0..s are zero."""
+        world.ensure_device_rng()
+        h = self.native_handle(world)
+        st = stream if stream is not None else N.stream_handle(world.device)
+        n, A = len(step_action_ptrs), len(world.agents)
+        outs = [self.alloc_outputs(world, h.obs_dim) for _ in range(n)]
+        io = N.SsRolloutIO()
+        acts = (N.c_vp * (n * A))(*[p for ptrs in step_action_ptrs for p in ptrs])
+        obs = (N.c_vp * n)(*[o.data_ptr() for o, _, _ in outs])
+        rew = (N.c_vp * n)(*[r.data_ptr() for _, r, _ in outs])
+        done = (N.c_vp * n)(*[d.data_ptr() for _, _, d in outs])
+        io.n_steps, io.actions, io.obs, io.rew, io.done = n, acts, obs, rew, done
+        io.obs_agent_stride = outs[0][0].shape[1] * outs[0][0].shape[2]
+        io.guard = guard.data_ptr() if guard is not None else None
+        io.check_actions = int(check_actions)
+        N.check(N.lib().ss_env_rollout(h.handle, world.buffers_ref(), ctypes.byref(io), st))
+        return outs
+
     # ---- reference hooks as kernel modes ----------------------------------
     def observe_all(self, world: World) -> list:
         obs, _, _ = self.launch(world, N.DO_OBS)

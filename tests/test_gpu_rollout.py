@@ -1,0 +1,98 @@
+"""The fused rollout kernel (ss_env_rollout): S consecutive steps of
+simple_spread / transport / reverse_transport in ONE launch, each env's
+state kept on chip between them.  Every intermediate StepResult, the final
+state and the step counters must equal eager Env.step bit for bit
+(env.py:209-235 per step), across the horizon, masked resets between
+replays and a NaN stop inside a replay."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2207_03530_b200 as S
+
+pytestmark = pytest.mark.gpu
+
+
+def state(e):
+    return e.world.state_array().cpu().numpy()
+
+
+def outs(r):
+    return r.obs + r.rewards + [r.dones]
+
+
+CASES = [("simple_spread", {}), ("simple_spread", {"n_agents": 1}), ("simple_spread", {"n_agents": 8}),
+         ("transport", {}), ("transport", {"n_agents": 7}), ("reverse_transport", {})]
+
+
+@pytest.mark.parametrize("name,ov", CASES)
+@pytest.mark.parametrize("S_", [2, 5, 16])
+def test_rollout_equals_eager(cuda, name, ov, S_):
+    B, horizon = 333, 7                   # the horizon falls inside a replay
+    a = S.Env(S.create_scenario(name, **ov), B, seed=4, device=cuda, validate=False, max_steps=horizon)
+    b = S.Env(S.create_scenario(name, **ov), B, seed=4, device=cuda, validate=False, max_steps=horizon)
+    A = len(a.agents)
+    g = torch.Generator(device=cuda)
+    g.manual_seed(11)
+    bufs = [torch.rand((A, B, 2), device=cuda, generator=g) * 2 - 1 for _ in range(3)]
+    graph = b.step_graph(bufs, steps_per_replay=S_, fused_rollout=True)
+    assert graph.fused_rollout and graph.launches_per_replay == 1
+    mask = torch.zeros(B, dtype=torch.bool, device=cuda)
+    mask[::5] = True
+    for rep in range(3):
+        i = rep % 3
+        rs = graph.rollout(i)
+        for s in range(S_):
+            ra = a.step(bufs[(i + s) % 3])
+            for x, y in zip(outs(ra), outs(rs[s])):
+                assert torch.equal(x, y), f"replay {rep} step {s}"
+        np.testing.assert_array_equal(state(a), state(b))
+        assert torch.equal(a.world.step_count, b.world.step_count)
+        a.reset_at(mask)
+        b.reset_at(mask)
+
+
+def test_rollout_nan_stops_mid_replay(cuda):
+    """validate=True: a NaN in step k of the replay stops the rollout kernel
+    before step k (state as after step k-1, like the eager step that raises)."""
+    B, S_ = 257, 6
+    ref = S.Env(S.create_scenario("simple_spread"), B, seed=6, device=cuda)
+    e = S.Env(S.create_scenario("simple_spread"), B, seed=6, device=cuda, validate=False)
+    A = len(e.agents)
+    g = torch.Generator(device=cuda)
+    g.manual_seed(2)
+    bufs = [torch.rand((A, B, 2), device=cuda, generator=g) * 2 - 1 for _ in range(2 * S_)]
+    graph = e.step_graph(bufs, steps_per_replay=S_, validate=True)
+    assert graph.fused_rollout and graph.launches_per_replay == 2   # scan + rollout
+    outs0 = graph.rollout(0)
+    graph.check()
+    for k in range(S_):
+        r = ref.step(bufs[k].clone())
+        for x, y in zip(outs(r), outs(outs0[k])):
+            assert torch.equal(x, y)
+    bufs[S_ + 3][2, 100, 1] = float("nan")
+    for k in range(S_, S_ + 3):
+        ref.step(bufs[k].clone())
+    graph.rollout(S_)
+    with pytest.raises(S.ContractViolation, match="NaN"):
+        graph.check()
+    np.testing.assert_array_equal(state(e), state(ref))
+    assert torch.equal(e.world.step_count, ref.world.step_count)
+
+
+def test_rollout_off_and_unsupported_fall_back_to_per_step(cuda):
+    """fused_rollout=False, S=1, physics sub-steps, or a scenario without a
+    rollout kernel: the per-step graph; None (default) takes it where the
+    scenario prefers it (simple_spread, not transport)."""
+    B = 64
+    for name, ov, S_, fused, want in [("simple_spread", {}, 4, False, False), ("simple_spread", {}, 1, True, False),
+                                      ("simple_spread", {"substeps": 2}, 4, True, False),
+                                      ("flocking", {}, 4, True, False), ("transport", {}, 4, True, True),
+                                      ("transport", {}, 4, None, False), ("simple_spread", {}, 4, None, True)]:
+        e = S.Env(S.create_scenario(name), B, seed=1, device=cuda, validate=False, **ov)
+        A = len(e.agents)
+        buf = torch.zeros((A, B, 2), device=cuda)
+        graph = e.step_graph(buf, steps_per_replay=S_, fused_rollout=fused)
+        assert graph.fused_rollout is want, name
+        assert graph.launches_per_replay == (1 if want else S_)
+        graph.step()

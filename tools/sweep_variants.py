@@ -1,6 +1,8 @@
 """Time the fused step kernel of each workload for several library variants.
 
-    [SWEEP_WORKLOADS=a,b] [SWEEP_ENVS=transport=1000000,...] python tools/sweep_variants.py LIB [LIB ...]
+    [SWEEP_WORKLOADS=a,b] [SWEEP_ENVS=transport=1000000,...] [SWEEP_S=10] python tools/sweep_variants.py LIB [LIB ...]
+
+SWEEP_S: steps per graph replay (a fused rollout launch where the world has one).
 
 Each LIB is loaded in a fresh subprocess (SS_LIB_PATH) and every workload
 is stepped with device-resident actions; prints the median per-launch time
@@ -27,7 +29,8 @@ for name in %(names)r:
     env = Env(create_scenario(scen, **ov), B, seed=0, device="cuda:0", validate=False)
     A = len(env.agents); O = env.observations()[0].shape[1]
     acts = [torch.rand((A, B, 2), device="cuda:0") * 2 - 1 for _ in range(2)]
-    g = env.step_graph(acts)
+    S = %(S)r
+    g = env.step_graph(acts, steps_per_replay=S)
     import time
     t_end = time.perf_counter() + 0.5          # clock soak before timing
     k = 0
@@ -40,9 +43,9 @@ for name in %(names)r:
     for k in range(40): g.step(k % 2)
     e.record()
     torch.cuda.synchronize()
-    ms = s.elapsed_time(e) / 40
-    bpe = bytes_per_env_step(scen, A, len(env.world.entities) - A, O)
-    out[name] = {"ms": ms, "frac": bpe * B / (ms / 1e3) / 1e9 / peaks()["hbm_gbs"]}
+    ms = s.elapsed_time(e) / (40 * S)
+    bpe = bytes_per_env_step(scen, A, len(env.world.entities) - A, O, S if g.fused_rollout else 1)
+    out[name] = {"ms": ms, "fused_rollout": g.fused_rollout, "frac": bpe * B / (ms / 1e3) / 1e9 / peaks()["hbm_gbs"]}
 print("RESULT " + json.dumps(out))
 """
 
@@ -54,7 +57,7 @@ def main() -> None:
         env = dict(os.environ, SS_LIB_PATH=str(Path(lib).resolve()))
         envs = dict((kv.split("=")[0], int(kv.split("=")[1])) for kv in os.environ.get("SWEEP_ENVS", "").split(",") if kv)
         code = (CHILD.replace("%(root)r", repr(str(ROOT))).replace("%(names)r", repr(names))
-                .replace("%(envs)r", repr(envs)))
+                .replace("%(envs)r", repr(envs)).replace("%(S)r", os.environ.get("SWEEP_S", "1")))
         res = subprocess.run([sys.executable, "-c", code],
                              env=env, capture_output=True, text=True)
         line = next((l for l in res.stdout.splitlines() if l.startswith("RESULT ")), None)
