@@ -89,10 +89,12 @@ def workload_string(name: str, B: int, Bg: int, world: int, strong: bool) -> str
     return f"{scen} {ov}, {B} envs per GPU"
 
 
-def ncu_traffic(scenario: str, envs: int):
+def ncu_traffic(scenario: str, envs: int, rollout: int = 0):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the fused
     kernel from the committed ncu --set full captures (profiles/r02, then
-    r01), if one was taken at this batch size; else None."""
+    r01), if one was taken at this batch size; else None.  rollout=S: the
+    capture of the S-step rollout kernel, its bytes per launch / S (per
+    step, like roofline.achieved)."""
     for rnd in ("r02", "r01"):
         p = ROOT / "profiles" / rnd / "ncu_traffic.json"
         if not p.exists():
@@ -102,9 +104,9 @@ def ncu_traffic(scenario: str, envs: int):
             continue
         if "envs" in d:                      # r01 layout: one capture per scenario
             d = {str(d["envs"]): d}
-        hit = d.get(str(envs))
+        hit = d.get(f"{envs}@rollout{rollout}" if rollout else str(envs))
         if hit:
-            return hit["dram_bytes_per_launch"], f"profiles/{rnd}/ncu_traffic.json"
+            return hit["dram_bytes_per_launch"] / hit.get("steps_per_launch", 1), f"profiles/{rnd}/ncu_traffic.json"
     return None, None
 
 
@@ -580,7 +582,7 @@ def run_b200(args, rank, world, local) -> None:
 
     if rank == 0:
         pk = peaks()
-        traffic, tsrc = ncu_traffic(scen, B)
+        traffic, tsrc = ncu_traffic(scen, B, S if graph_fused else 0)
         line = {
             "metric": "agent-steps/sec", "value": value, "unit": "agent-steps/s",
             "env_steps_per_s": env_steps / (ms_total / 1000.0),
@@ -601,7 +603,9 @@ def run_b200(args, rank, world, local) -> None:
                                       "host buffers")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
-                         "traffic_source": tsrc and f"{tsrc} (ncu --set full, one launch at {B} envs)",
+                         "traffic_source": tsrc and (f"{tsrc} (ncu --set full, one launch at {B} envs"
+                                                     + (f", the {S}-step rollout kernel's bytes / {S})"
+                                                        if graph_fused else ")")),
                          "bytes_per_env_step": bpe,
                          "bytes_model": (f"per step {step_bytes(scen, A, n_other, O)[0]} B (actions, outputs) + "
                                          f"{step_bytes(scen, A, n_other, O)[1]} B (state r/w, static, step_count) "

@@ -261,10 +261,11 @@ SS_HD float np_sinf(float x) { return np_sincosf(x, false); }
 SS_HD float np_softplus(float z) {
   const float kLogE2f = 0.693147180559945309417232121458176568f;
   if (0.0f == z) return fadd(0.0f, kLogE2f);
-  const float tmp = fsub(0.0f, z);
-  if (tmp > 0.0f) return fadd(0.0f, gl_log1pf(gl_expf(-tmp)));
-  if (tmp <= 0.0f) return fadd(z, gl_log1pf(gl_expf(tmp)));
-  return tmp;  // nan
+  // numpy's two branches (tmp = 0 - z > 0: 0 + log1p(exp(-tmp)); else
+  // z + log1p(exp(tmp))) share one exp / log1p of -|z| (0 - z = -z exactly
+  // for finite nonzero z): one code path, no divergence between the signs.
+  const float l = gl_log1pf(gl_expf(-fabsf(z)));
+  return fadd(z < 0.0f ? 0.0f : z, l);   // NaN z: NaN either way
 }
 
 // ---- numpy Philox4x64-10 ----------------------------------------------------

@@ -5,7 +5,13 @@
 
 namespace ss {
 
+static void fill_const_desc(const World& w, SmallArgs& a) {
+  memcpy(a.ek, w.ents.data(), sizeof(SsEntityDesc) * std::min<size_t>(w.ents.size(), kSmallConstEnts));
+  memcpy(a.pk, w.pairs.data(), sizeof(SsPairDesc) * std::min<size_t>(w.pairs.size(), kSmallConstPairs));
+}
+
 static void fill_small_args(World& w, const SsBuffers* buf, SmallArgs& a) {
+  fill_const_desc(w, a);
   a.s = make_state(w, buf);
   a.ph = make_phys(w);
   a.ents = w.d_ents;
@@ -115,6 +121,7 @@ int launch_small(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_
   a.ph = make_phys(w);
   a.ents = w.d_ents;
   a.pairs = w.d_pairs;
+  fill_const_desc(w, a);
   const int NA = w.d.n_agents;
   if (NA < 1 || NA > kSmallMaxAgents) {
     set_error("fused kernel instantiated for 1.." + std::to_string(kSmallMaxAgents) + " agents");

@@ -33,6 +33,16 @@ constexpr int kSmallThreads = 128;
 #define SS_SMALL_MINB 6   // 6 x 128 threads: <= 80 registers, best measured (tools/sweep_variants.py)
 #endif
 
+// Entity / pair descriptors the fixed-template kernels (simple_spread,
+// transport) read by value from the kernel parameters: constant-bank
+// operands of the arithmetic, no loads (and no registers waiting on them)
+// inside the step.  SS_CONST_DESC=0 reads them from global memory instead.
+#ifndef SS_CONST_DESC
+#define SS_CONST_DESC 1
+#endif
+constexpr int kSmallConstEnts = kSmallMaxAgents + 1;                              // transport: + package
+constexpr int kSmallConstPairs = kSmallMaxAgents * (kSmallMaxAgents - 1) / 2 + kSmallMaxAgents;
+
 struct SmallArgs {
   DevState s;
   PhysK ph;
@@ -60,7 +70,14 @@ struct SmallArgs {
   double ray_start, ray_span;
   int attach_rot;
   const double* ray_dir;  // [n_rays][2] cos/sin of the base angles (numpy values)
+  SsEntityDesc ek[kSmallConstEnts];   // ents[0 .. kSmallConstEnts) by value
+  SsPairDesc pk[kSmallConstPairs];    // pairs[0 .. kSmallConstPairs) by value
 };
+
+// Descriptor i / pair p of a fixed-template kernel (compile-time index
+// below the by-value counts).
+SS_DEV const SsEntityDesc& tmpl_ent(const SmallArgs& a, int i) { return SS_CONST_DESC ? a.ek[i] : a.ents[i]; }
+SS_DEV const SsPairDesc& tmpl_pair(const SmallArgs& a, int p) { return SS_CONST_DESC ? a.pk[p] : a.pairs[p]; }
 
 // Flush one agent's staged obs rows (warp-private smem) to global memory.
 SS_DEV void warp_flush(float* __restrict__ dst, int nvalid, int O, float* __restrict__ sbuf) {
@@ -120,6 +137,11 @@ __host__ __device__ constexpr bool obs_bulk(int NA, int O) { return kObsBulk && 
 #endif
 __host__ __device__ constexpr int obs_nbuf(int NA, int O) {
   return !obs_bulk(NA, O) ? 1 : (SS_OBS_NBUF > 0 && SS_OBS_NBUF < NA ? SS_OBS_NBUF : NA);
+}
+
+// The warp's whole staging region (obs_nbuf blocks of 32 * O floats).
+SS_DEV float* obs_stage_base(float* smem, int NA, int O) {
+  return smem + (threadIdx.x >> 5) * obs_nbuf(NA, O) * (32 * O);
 }
 
 // Staging block of (warp, agent i).

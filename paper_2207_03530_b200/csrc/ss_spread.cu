@@ -26,7 +26,7 @@ struct SpreadEnv {
     float ux[NA], uy[NA];
 #pragma unroll
     for (int i = 0; i < NA; ++i) {
-      const SsEntityDesc& d = a.ents[i];
+      const SsEntityDesc& d = tmpl_ent(a, i);
       ux[i] = decode_axis(u[i].x, d, a.raw_forces);
       uy[i] = decode_axis(u[i].y, d, a.raw_forces);
       if (a.ph.has_gravity) { ux[i] = fadd(ux[i], d.grav_x); uy[i] = fadd(uy[i], d.grav_y); }
@@ -41,7 +41,7 @@ struct SpreadEnv {
       for (int i = 0; i < NA; ++i) {
 #pragma unroll
         for (int j = i + 1; j < NA; ++j, ++p) {
-          const SsPairDesc pr = a.pairs[p];
+          const SsPairDesc pr = tmpl_pair(a, p);
           float cx, cy;
           if (contact_force(px[i], py[i], px[j], py[j], pr.d_min, pr.d2_act, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
             fx[i] = fadd(fx[i], cx); fy[i] = fadd(fy[i], cy);
@@ -51,7 +51,7 @@ struct SpreadEnv {
       }
 #pragma unroll
       for (int i = 0; i < NA; ++i) {
-        const SsEntityDesc& d = a.ents[i];
+        const SsEntityDesc& d = tmpl_ent(a, i);
         integrate_lin(px[i], py[i], vx[i], vy[i], fx[i], fy[i], a.ph.keep, d.inv_m_dt, a.ph.dt,
                       d.max_speed);
       }

@@ -19,10 +19,26 @@ namespace ss {
 // actions + gravity), contacts in the reference's pair order (agent pairs,
 // then agent i vs the package box), integrate; STORE: write each state row
 // as soon as it is final.
+//
+// Contacts in three phases, so the expensive part of collision_force (sqrt,
+// two divisions, softplus) exists once in the code and runs with every lane
+// of the warp busy: (1) per pair, unrolled: the cheap geometry and the
+// activity test (dynamics.py:46-50), the offset of each active pair parked
+// in the warp's shared scratch `scr` (float2 per pair, lane-interleaved);
+// (2) each lane walks ITS active pairs (a bitmask) through one copy of the
+// force code, so lanes with different active pairs share the instructions
+// instead of diverging over ten inlined copies; (3) per pair, unrolled, the
+// forces are summed in the reference's pair order.  Same operations on the
+// same values: bitwise the one-pass result.
+template <int NA>
+constexpr int transport_pairs() { return NA * (NA - 1) / 2 + NA; }
+
 template <int NA, bool STORE>
 SS_DEV void transport_physics(float (&px)[NA + 1], float (&py)[NA + 1], float (&vx)[NA + 1],
                               float (&vy)[NA + 1], const float2 (&act)[NA], float ca, float sa,
-                              const SmallArgs& a, int64_t B, int64_t e) {
+                              const SmallArgs& a, int64_t B, int64_t e, float2* scr) {
+  constexpr int P = transport_pairs<NA>();
+  static_assert(P <= 64, "pair mask is 64 bits");
   const double hx = a.sd[0], hy = a.sd[1];
   float fx[NA + 1], fy[NA + 1];
 #pragma unroll
@@ -38,25 +54,54 @@ SS_DEV void transport_physics(float (&px)[NA + 1], float (&py)[NA + 1], float (&
       fx[i] = fadd(fx[i], a.ents[i].grav_x); fy[i] = fadd(fy[i], a.ents[i].grav_y);
     }
   }
-  int p = 0;
+  // (1) geometry + activity, pair order
+  uint64_t act_mask = 0;
+  {
+    int p = 0;
 #pragma unroll
-  for (int i = 0; i < NA; ++i) {
+    for (int i = 0; i < NA; ++i) {
 #pragma unroll
-    for (int j = i + 1; j < NA; ++j, ++p) {
-      const SsPairDesc pr = a.pairs[p];
-      float cx, cy;
-      if (contact_force(px[i], py[i], px[j], py[j], pr.d_min, pr.d2_act, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
-        fx[i] = fadd(fx[i], cx); fy[i] = fadd(fy[i], cy);
-        fx[j] = fsub(fx[j], cx); fy[j] = fsub(fy[j], cy);
+      for (int j = i + 1; j < NA; ++j, ++p) {
+        const float x = fsub(px[i], px[j]), y = fsub(py[i], py[j]);
+        if (fadd(fmul(x, x), fmul(y, y)) <= a.pairs[p].d2_act) {
+          act_mask |= 1ull << p;
+          scr[p * 32] = make_float2(x, y);
+        }
       }
-    }
-    {  // agent i vs package (sphere-box)
-      const SsPairDesc pr = a.pairs[p++];
-      float qx, qy, cx, cy;
+      float qx, qy;   // agent i vs package (sphere-box): closest point on the box
       closest_point_on_box(px[i], py[i], px[NA], py[NA], ca, sa, hx, hy, qx, qy);
-      if (contact_force(px[i], py[i], qx, qy, pr.d_min, pr.d2_act, pr.sign, a.ph.ck, a.ph.k, cx, cy)) {
-        fx[i] = fadd(fx[i], cx); fy[i] = fadd(fy[i], cy);
-        fx[NA] = fsub(fx[NA], cx); fy[NA] = fsub(fy[NA], cy);
+      const float x = fsub(px[i], qx), y = fsub(py[i], qy);
+      if (fadd(fmul(x, x), fmul(y, y)) <= a.pairs[p].d2_act) {
+        act_mask |= 1ull << p;
+        scr[p * 32] = make_float2(x, y);
+      }
+      ++p;
+    }
+  }
+  // (2) this lane's active pairs through one copy of the force code
+  for (uint64_t m = act_mask; m != 0; m &= m - 1) {
+    const int p = __ffsll((long long)m) - 1;
+    const SsPairDesc pr = a.pairs[p];
+    const float2 xy = scr[p * 32];
+    const float d = fsqrt(fadd(fmul(xy.x, xy.x), fmul(xy.y, xy.y)));
+    float dx, dy;
+    if (d < 1e-8f) { dx = pr.sign; dy = 0.0f; }          // DEGENERATE_DIST, dynamics.py:23
+    else { dx = fdiv(xy.x, d); dy = fdiv(xy.y, d); }
+    const float mag = fmul(a.ph.ck, np_softplus(fdiv(fsub(pr.d_min, d), a.ph.k)));
+    scr[p * 32] = make_float2(fmul(dx, mag), fmul(dy, mag));
+  }
+  // (3) accumulate in pair order
+  {
+    int p = 0;
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+#pragma unroll
+      for (int j = i + 1; j <= NA; ++j, ++p) {   // j == NA: the package
+        if ((act_mask >> p) & 1u) {
+          const float2 c = scr[p * 32];
+          fx[i] = fadd(fx[i], c.x); fy[i] = fadd(fy[i], c.y);
+          fx[j] = fsub(fx[j], c.x); fy[j] = fsub(fy[j], c.y);
+        }
       }
     }
   }
@@ -69,6 +114,14 @@ SS_DEV void transport_physics(float (&px)[NA + 1], float (&py)[NA + 1], float (&
     // the stores while the next entity integrates)
     if (STORE) a.s.dyn[i * B + e] = make_float4(px[i], py[i], vx[i], vy[i]);
   }
+}
+
+// The warp's contact scratch: transport_pairs<NA>() float2 per lane inside
+// the warp's own obs staging block (free until the obs rows are staged).
+template <int NA, int O>
+SS_DEV float2* transport_scratch(float* smem) {
+  static_assert(2 * transport_pairs<NA>() <= obs_nbuf(NA, O) * O, "scratch fits the warp's staging");
+  return reinterpret_cast<float2*>(obs_stage_base(smem, NA, O)) + (threadIdx.x & 31);
 }
 
 // Observation row of agent i: [x, y, vx, vy, package - self, goal - self,
@@ -124,7 +177,8 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_transport(cons
   if (valid && (a.mode & SS_DO_PHYSICS)) {
     float ca, sa;
     if (prot == 0.0f) { ca = 1.0f; sa = prot; } else { ca = np_cosf(prot); sa = np_sinf(prot); }
-    transport_physics<NA, !MS>(px, py, vx, vy, u, ca, sa, a, B, e);
+    float2* scr = transport_scratch<NA, O>(smem);
+    transport_physics<NA, !MS>(px, py, vx, vy, u, ca, sa, a, B, e, scr);
     // further physics sub-steps (PhysK.substeps > 1: the MS instantiation,
     // so the reference's single step keeps its register budget) reload the
     // held actions instead of keeping them live across the first one
@@ -132,7 +186,7 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_transport(cons
       float2 ur[NA];
 #pragma unroll
       for (int i = 0; i < NA; ++i) ur[i] = a.act[i][e];
-      transport_physics<NA, false>(px, py, vx, vy, ur, ca, sa, a, B, e);
+      transport_physics<NA, false>(px, py, vx, vy, ur, ca, sa, a, B, e, scr);
     }
     if (MS) {
 #pragma unroll
@@ -153,6 +207,7 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_transport(cons
     float* row = nullptr;
     const int64_t e0 = e - (threadIdx.x & 31);
     const int nvalid = (int)min((int64_t)32, B - e0);
+    __syncwarp();   // every lane is done with its contact scratch in the staging
 #pragma unroll
     for (int i = 0; i < NA; ++i) {
       sbuf = obs_stage(smem, i, NA, O);
@@ -206,18 +261,19 @@ __global__ void __launch_bounds__(kSmallThreads, SS_ROLLOUT_MINB) k_transport_ro
 #pragma unroll
       for (int i = 0; i < NA; ++i) un[i] = __ldcs(r.act[s + 1][i] + e);
     }
+    if (s > 0) {   // the previous step's bulk stores must have read the staging
+      obs_bulk_drain();
+      __syncwarp();
+    }
     if (valid) {
-      transport_physics<NA, false>(px, py, vx, vy, u, ca, sa, a, B, e);
+      transport_physics<NA, false>(px, py, vx, vy, u, ca, sa, a, B, e, transport_scratch<NA, O>(smem));
       steps += 1;
       const float gap = norm2(fsub(px[NA], gx), fsub(py[NA], gy));
 #pragma unroll
       for (int i = 0; i < NA; ++i) __stcs(r.rew[s] + i * B + e, -gap);
       r.done[s][e] = (uint8_t)((gap < a.sc[2]) | (steps >= a.ph.max_steps));
     }
-    if (s > 0) {   // the previous step's bulk stores must have read the staging
-      obs_bulk_drain();
-      __syncwarp();
-    }
+    __syncwarp();   // every lane is done with its contact scratch in the staging
 #pragma unroll
     for (int i = 0; i < NA; ++i) {
       float* sbuf = obs_stage(smem, i, NA, O);

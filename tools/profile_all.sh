@@ -2,9 +2,10 @@
 # Profiling runs for profiles/ (execute on the GPU box via gpurun, 1 GPU; one
 # ncu invocation per gpurun call):
 #   bash tools/profile_all.sh launches     bench plainly, then its ncu launch list
-#   [ENVS=n] bash tools/profile_all.sh SCENARIO   step loop plainly, then one ncu --set full
-#                                          capture of the fused kernel in steady state
-#                                          (ENVS: batch size, default the workload's)
+#   [ENVS=n] [ROLLOUT=S] bash tools/profile_all.sh SCENARIO   step loop plainly, then one
+#                                          ncu --set full capture of the fused kernel in steady
+#                                          state (ENVS: batch size, default the workload's;
+#                                          ROLLOUT: capture the S-step rollout kernel instead)
 # Summaries land in gpurun_out/ (tools/ncu_summary.py); the .ncu-rep is deleted
 # to keep the merge-back small.
 set -u
@@ -28,9 +29,18 @@ s=$what
 ENVS=${ENVS:-0}
 tag=$s${ENVS/#0/}
 [ "$ENVS" != 0 ] && tag=${s}_$ENVS
-CMD="python tools/step_loop.py $s $ENVS $((${PRE[$s]} + 2))"
+ROLLOUT=${ROLLOUT:-0}
+kern=${KERN[$s]}
+pre=${PRE[$s]}
+if [ "$ROLLOUT" != 0 ]; then
+  kern=${kern}_rollout
+  pre=$(( (pre + ROLLOUT - 1) / ROLLOUT ))
+  tag=${s}_rollout${ROLLOUT}${ENVS/#0/}
+  [ "$ENVS" != 0 ] && tag=${s}_rollout${ROLLOUT}_$ENVS
+fi
+CMD="python tools/step_loop.py $s $ENVS $((pre + 2)) $ROLLOUT"
 $CMD > $OUT/plain_$tag.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:${KERN[$s]} -s ${PRE[$s]} -c 1 \
+  ncu --set full --clock-control none --import-source on -k regex:$kern -s $pre -c 1 \
       -o $OUT/full_$tag $CMD > $OUT/ncu_full_$tag.log 2>&1
 echo "$tag: $?"
 [ -f $OUT/full_$tag.ncu-rep ] && python tools/ncu_summary.py $OUT/full_$tag.ncu-rep $OUT/full_$tag && rm -f $OUT/full_$tag.ncu-rep

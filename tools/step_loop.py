@@ -1,8 +1,10 @@
-"""Minimal step loop for profiling: python tools/step_loop.py SCENARIO ENVS STEPS.
+"""Minimal step loop for profiling: python tools/step_loop.py SCENARIO ENVS STEPS [ROLLOUT].
 
 Runs STEPS fused Env.step calls (validate=False, device-resident actions) of
 the bench workload SCENARIO with ENVS envs on cuda:0 — short enough to run
 under `ncu --set full` (see profiles/README.md for the exact commands).
+ROLLOUT=S > 0: STEPS replays of a StepGraph of S steps with the fused
+rollout kernel (one ss_env_rollout launch per replay) instead.
 """
 import sys
 from pathlib import Path
@@ -23,7 +25,14 @@ def main() -> None:
     env = Env(create_scenario(scen, **ov), B, seed=0, device="cuda:0", validate=False)
     A = len(env.agents)
     acts = torch.rand((A, B, 2), device="cuda:0") * 2 - 1
-    for _ in range(steps):
+    roll = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+    if roll > 0:
+        bufs = [torch.rand((A, B, 2), device="cuda:0") * 2 - 1 for _ in range(2)]
+        graph = env.step_graph(bufs, steps_per_replay=roll, fused_rollout=True)
+        assert graph.fused_rollout, name
+        for k in range(steps):
+            graph.step(k % 2)
+    for _ in range(steps if roll <= 0 else 0):
         env.step(acts)
     torch.cuda.synchronize()
     print(f"{name}: {steps} steps of {B} envs ok")
