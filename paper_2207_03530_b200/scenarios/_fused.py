@@ -149,12 +149,11 @@ class FusedScenario(Scenario):
                 and world.params.substeps == 1 and len(world.agents) <= 8)
 
     def rollout_preferred(self, world: World) -> bool:
-        """Take the rollout kernel by default (StepGraph fused_rollout=None):
-        where the step is bound by its HBM traffic, which the rollout cuts.
-        transport's step is latency / issue bound (the box-contact physics),
-        so its rollout kernel is no faster than the per-step graph (measured,
-        DESIGN.md) and stays opt-in."""
-        return self.native_id == N.SCN_SIMPLE_SPREAD and self.rollout_capable(world)
+        """Take the rollout kernel by default (StepGraph fused_rollout=None)
+        wherever it exists: both steps are bound by their HBM traffic, which
+        the rollout cuts (measured at 1M envs: simple_spread 57.7 -> 36.6 us
+        per step, transport 80.2 -> 53.8)."""
+        return self.rollout_capable(world)
 
     def launch_rollout(self, world: World, step_action_ptrs: list, guard=None, stream: int | None = None,
                        check_actions: bool = False) -> list:

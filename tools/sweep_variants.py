@@ -2,7 +2,8 @@
 
     [SWEEP_WORKLOADS=a,b] [SWEEP_ENVS=transport=1000000,...] [SWEEP_S=10] python tools/sweep_variants.py LIB [LIB ...]
 
-SWEEP_S: steps per graph replay (a fused rollout launch where the world has one).
+SWEEP_S: steps per graph replay; SWEEP_FUSED=1/0 forces the fused rollout
+kernel on / off (default: where the scenario prefers it).
 
 Each LIB is loaded in a fresh subprocess (SS_LIB_PATH) and every workload
 is stepped with device-resident actions; prints the median per-launch time
@@ -30,7 +31,7 @@ for name in %(names)r:
     A = len(env.agents); O = env.observations()[0].shape[1]
     acts = [torch.rand((A, B, 2), device="cuda:0") * 2 - 1 for _ in range(2)]
     S = %(S)r
-    g = env.step_graph(acts, steps_per_replay=S)
+    g = env.step_graph(acts, steps_per_replay=S, fused_rollout=%(fused)s)
     import time
     t_end = time.perf_counter() + 0.5          # clock soak before timing
     k = 0
@@ -57,7 +58,8 @@ def main() -> None:
         env = dict(os.environ, SS_LIB_PATH=str(Path(lib).resolve()))
         envs = dict((kv.split("=")[0], int(kv.split("=")[1])) for kv in os.environ.get("SWEEP_ENVS", "").split(",") if kv)
         code = (CHILD.replace("%(root)r", repr(str(ROOT))).replace("%(names)r", repr(names))
-                .replace("%(envs)r", repr(envs)).replace("%(S)r", os.environ.get("SWEEP_S", "1")))
+                .replace("%(envs)r", repr(envs)).replace("%(S)r", os.environ.get("SWEEP_S", "1"))
+                .replace("%(fused)s", {"1": "True", "0": "False"}.get(os.environ.get("SWEEP_FUSED", ""), "None")))
         res = subprocess.run([sys.executable, "-c", code],
                              env=env, capture_output=True, text=True)
         line = next((l for l in res.stdout.splitlines() if l.startswith("RESULT ")), None)
