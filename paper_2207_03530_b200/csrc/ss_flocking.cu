@@ -462,12 +462,12 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_flocking(const
 #ifndef SS_FLOCK_WARPS
 #define SS_FLOCK_WARPS 40   // resident warps per SM the register budget is sized for
 #endif
-template <int NA>
-__global__ void __launch_bounds__(32 * NA, (SS_FLOCK_WARPS / NA < 32 ? SS_FLOCK_WARPS / NA : 32))
-    k_flocking_w(const SmallArgs a, const FlockLidarK lk) {
+// ROLL: the fused rollout (RolloutArgs *ro, SS_MODE_STEP): the steps of
+// the replay in one launch, the agents' rows kept in registers and the
+// beacon / rocks staged once; the per-step pointers come from ro.
+template <int NA, bool ROLL>
+SS_DEV void flocking_w_body(const SmallArgs& a, const FlockLidarK& lk, const RolloutArgs* ro) {
   extern __shared__ __align__(16) float smem_w[];
-  grid_dep_sync();
-  if (guard_tripped(a.guard, a.guard_n)) return;
   const int NO = a.si[4];
   const int O = a.obs_dim;
   const int P = O | 1;
@@ -499,17 +499,27 @@ __global__ void __launch_bounds__(32 * NA, (SS_FLOCK_WARPS / NA < 32 ? SS_FLOCK_
   }
   float4 me = make_float4(0.f, 0.f, 0.f, 0.f);
   int64_t steps = 0;
-  float2 u = make_float2(0.f, 0.f);
+  const int mode = ROLL ? SS_MODE_STEP : a.mode;
   if (valid) {
     // every global load of the step issued up front
     me = a.s.dyn[i * B + e];
-    if (a.mode & (SS_DO_COUNT | SS_DO_DONE)) steps = a.s.step_count[e];
-    if (a.mode & SS_DO_PHYSICS) u = a.act[i][e];
-    sag[i * 32 + lane] = me;
+    if (mode & (SS_DO_COUNT | SS_DO_DONE)) steps = a.s.step_count[e];
     for (int k = i; k < 1 + NO; k += NA) sst[k * 32 + lane] = a.s.stat[k * B + e];
   }
+  const int n_steps = ROLL ? rollout_len(ro->guard, ro->n_steps) : 1;
+  for (int step = 0; step < n_steps; ++step) {
+  const float2* act_i = ROLL ? ro->act[step][i] : a.act[i];
+  float* const obs_out = ROLL ? ro->obs[step] : a.obs;
+  float* const rew_out = ROLL ? ro->rew[step] : a.rew;
+  uint8_t* const done_out = ROLL ? ro->done[step] : a.done;
+  float2 u = make_float2(0.f, 0.f);
+  if (valid && (mode & SS_DO_PHYSICS)) u = act_i[e];
+  // (rollout) every warp is done with the previous step's rows, positions
+  // and lidar queue before the pre-step copy overwrites the rows region
+  if (ROLL && step > 0) __syncthreads();
+  if (valid) sag[i * 32 + lane] = me;
   __syncthreads();
-  if (a.mode & SS_DO_PHYSICS) {
+  if (mode & SS_DO_PHYSICS) {
     const SsEntityDesc& d = a.ents[i];
     float ux = decode_axis(u.x, d, a.raw_forces), uy = decode_axis(u.y, d, a.raw_forces);
     if (a.ph.has_gravity) { ux = fadd(ux, d.grav_x); uy = fadd(uy, d.grav_y); }
@@ -549,13 +559,13 @@ __global__ void __launch_bounds__(32 * NA, (SS_FLOCK_WARPS / NA < 32 ? SS_FLOCK_
     integrate_lin(me.x, me.y, me.z, me.w, fx, fy, a.ph.keep, d.inv_m_dt, a.ph.dt, d.max_speed);
     }
     }
-    if (valid) a.s.dyn[i * B + e] = me;
+    if (valid && !ROLL) a.s.dyn[i * B + e] = me;
   }
   if (valid) spos[i * 32 + lane] = make_float2(me.x, me.y);
   __syncthreads();                       // post-step positions of every agent staged
-  if (valid && (a.mode & SS_DO_COUNT)) { steps += 1; if (i == 0) a.s.step_count[e] = steps; }
+  if (valid && (mode & SS_DO_COUNT)) { steps += 1; if (i == 0 && !ROLL) a.s.step_count[e] = steps; }
   const float2 beacon = valid ? sst[lane] : make_float2(0.f, 0.f);
-  if (valid && (a.mode & SS_DO_REWARD)) {
+  if (valid && (mode & SS_DO_REWARD)) {
     const float pen = a.sc[2], thr2_aa = a.sc[3], thr2_ar = a.sc[4];
     const float gap = norm2(fsub(me.x, beacon.x), fsub(me.y, beacon.y));
     float ca = 0.0f, cr = 0.0f;
@@ -569,10 +579,10 @@ __global__ void __launch_bounds__(32 * NA, (SS_FLOCK_WARPS / NA < 32 ? SS_FLOCK_
       const float2 q = sst[(1 + r) * 32 + lane];
       cr = fadd(cr, sqnorm(fsub(me.x, q.x), fsub(me.y, q.y)) <= thr2_ar ? 1.0f : 0.0f);
     }
-    __stcs(a.rew + i * B + e, fsub(-gap, fmul(pen, fadd(ca, cr))));
+    __stcs(rew_out + i * B + e, fsub(-gap, fmul(pen, fadd(ca, cr))));
   }
-  if (valid && i == 0 && (a.mode & SS_DO_DONE)) a.done[e] = (uint8_t)(steps >= a.ph.max_steps);
-  if (a.mode & SS_DO_OBS) {
+  if (valid && i == 0 && (mode & SS_DO_DONE)) done_out[e] = (uint8_t)(steps >= a.ph.max_steps);
+  if (mode & SS_DO_OBS) {
     float* row = srow + lane * P;
     if (valid) {
       row[0] = me.x; row[1] = me.y; row[2] = me.z; row[3] = me.w;
@@ -638,8 +648,30 @@ __global__ void __launch_bounds__(32 * NA, (SS_FLOCK_WARPS / NA < 32 ? SS_FLOCK_
         }
       }
     }
-    if (nvalid > 0) warp_flush_padded(a.obs + i * a.obs_stride + e0 * O, nvalid, O, P, srow);
+    if (nvalid > 0) warp_flush_padded(obs_out + i * a.obs_stride + e0 * O, nvalid, O, P, srow);
   }
+  }   // steps
+  if (ROLL && valid) {
+    a.s.dyn[i * B + e] = me;
+    if (i == 0) a.s.step_count[e] = steps;
+  }
+}
+
+template <int NA>
+__global__ void __launch_bounds__(32 * NA, (SS_FLOCK_WARPS / NA < 32 ? SS_FLOCK_WARPS / NA : 32))
+    k_flocking_w(const SmallArgs a, const FlockLidarK lk) {
+  grid_dep_sync();
+  if (guard_tripped(a.guard, a.guard_n)) return;
+  flocking_w_body<NA, false>(a, lk, nullptr);
+}
+
+// flocking, fused open-loop rollout (SsRolloutIO): ro.n_steps steps of
+// k_flocking_w's work per launch, each env's agents kept on chip between them.
+template <int NA>
+__global__ void __launch_bounds__(32 * NA, (SS_FLOCK_WARPS / NA < 32 ? SS_FLOCK_WARPS / NA : 32))
+    k_flocking_w_rollout(const RolloutArgs ro, const FlockLidarK lk) {
+  grid_dep_sync();
+  flocking_w_body<NA, true>(ro.a, lk, &ro);
 }
 
 inline size_t flocking_w_smem(int NA, int NO, int n_rays, int O) {
@@ -649,15 +681,13 @@ inline size_t flocking_w_smem(int NA, int NO, int n_rays, int O) {
          (size_t)(1 + NO) * 32 * sizeof(float2) + (rows > pre ? rows : pre);
 }
 
-int launch_flocking(World& w, SmallArgs& a, cudaStream_t st) {
-  const int NA = w.d.n_agents;
-  const int64_t B = w.d.batch;
-  const unsigned grid = (unsigned)((B + kSmallThreads - 1) / kSmallThreads);
-      if (w.d.si[4] > kFlockMaxRocks) {
+// Lidar constants of a flocking launch (a's lidar fields, the screens and
+// the uniform fan); SS_OK or an error status.
+static int flock_setup(World& w, SmallArgs& a, FlockLidarK& lk) {
+  if (w.d.si[4] > kFlockMaxRocks) {
     set_error("flocking fused kernel supports at most 6 obstacles");
     return SS_ERR_UNSUPPORTED;
   }
-  FlockLidarK lk;
   lk.r2_agent = w.d.sd[0];
   lk.r2_rock = w.d.sd[1];
   lk.agent = make_screen(w.d.sd[2], w.d.lidar_max_range);
@@ -686,8 +716,43 @@ int launch_flocking(World& w, SmallArgs& a, cudaStream_t st) {
     lk.fan.all = a.n_rays >= 32 ? 0xffffffffu : ((1u << a.n_rays) - 1u);
     lk.fan.full = span == two_pi && lk.fan.period == (float)a.n_rays;
   }
+  return SS_OK;
+}
+
+static bool flock_legacy() {
   static const bool legacy = std::getenv("SS_FLOCK_THREAD_PER_ENV") != nullptr;
-  if (!legacy) {
+  return legacy;
+}
+
+int launch_flocking_rollout(World& w, RolloutArgs& r, cudaStream_t st) {
+  FlockLidarK lk;
+  const int rc = flock_setup(w, r.a, lk);
+  if (rc != SS_OK) return rc;
+  if (flock_legacy()) { set_error("no flocking rollout on the thread-per-env kernel"); return SS_ERR_UNSUPPORTED; }
+  const int NA = w.d.n_agents;
+  const size_t wshmem = flocking_w_smem(NA, w.d.si[4], r.a.n_rays, w.d.obs_dim);
+  const unsigned wgrid = (unsigned)((w.d.batch + 31) / 32);
+#define SS_CASE(n)                                                                                        \
+  case n:                                                                                                 \
+    if (wshmem > 48 * 1024)                                                                               \
+      cudaFuncSetAttribute(k_flocking_w_rollout<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wshmem); \
+    launch_step(k_flocking_w_rollout<n>, dim3(wgrid), dim3(32 * n), wshmem, st, r, lk);                  \
+    break;
+  switch (NA) { SS_CASE(1) SS_CASE(2) SS_CASE(3) SS_CASE(4) SS_CASE(5) SS_CASE(6) SS_CASE(7) SS_CASE(8) }
+#undef SS_CASE
+  return cuda_status(cudaGetLastError(), "flocking rollout launch");
+}
+
+int launch_flocking(World& w, SmallArgs& a, cudaStream_t st) {
+  const int NA = w.d.n_agents;
+  const int64_t B = w.d.batch;
+  const unsigned grid = (unsigned)((B + kSmallThreads - 1) / kSmallThreads);
+  FlockLidarK lk;
+  {
+    const int rc = flock_setup(w, a, lk);
+    if (rc != SS_OK) return rc;
+  }
+  if (!flock_legacy()) {
     // warp per agent (k_flocking_w): 32 envs per CTA of NA warps
     const size_t wshmem = flocking_w_smem(NA, w.d.si[4], a.n_rays, w.d.obs_dim);
     const unsigned wgrid = (unsigned)((B + 31) / 32);

@@ -88,7 +88,8 @@ static int launch_check_rollout(World& w, const RolloutArgs& r, int* guard, cuda
 
 int launch_rollout(World& w, const SsBuffers* buf, const SsRolloutIO* io, cudaStream_t st) {
   const int NA = w.d.n_agents;
-  const bool capable = (w.d.scenario == SS_SCN_SIMPLE_SPREAD || w.d.scenario == SS_SCN_TRANSPORT) &&
+  const bool capable = (w.d.scenario == SS_SCN_SIMPLE_SPREAD || w.d.scenario == SS_SCN_TRANSPORT ||
+                        w.d.scenario == SS_SCN_FLOCKING) &&
                        NA >= 1 && NA <= kSmallMaxAgents && w.d.substeps <= 1 && w.d.n_joints == 0;
   if (!capable) {
     set_error("no fused rollout kernel for this world (take the per-step path)");
@@ -111,7 +112,11 @@ int launch_rollout(World& w, const SsBuffers* buf, const SsRolloutIO* io, cudaSt
     const int rc = launch_check_rollout(w, r, io->guard, st);
     if (rc != SS_OK) return rc;
   }
-  return w.d.scenario == SS_SCN_SIMPLE_SPREAD ? launch_spread_rollout(w, r, st) : launch_transport_rollout(w, r, st);
+  switch (w.d.scenario) {
+    case SS_SCN_SIMPLE_SPREAD: return launch_spread_rollout(w, r, st);
+    case SS_SCN_TRANSPORT: return launch_transport_rollout(w, r, st);
+    default: return launch_flocking_rollout(w, r, st);
+  }
 }
 
 int launch_small(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_t st) {

@@ -241,6 +241,7 @@ SS_DEV int rollout_len(const int* g, int n) {
 
 int launch_spread_rollout(World& w, RolloutArgs& r, cudaStream_t st);
 int launch_transport_rollout(World& w, RolloutArgs& r, cudaStream_t st);
+int launch_flocking_rollout(World& w, RolloutArgs& r, cudaStream_t st);
 
 // Host launchers, one per translation unit (a: filled by launch_small; grid /
 // shmem derived from it).  Each returns an SsStatus.

@@ -407,7 +407,7 @@ class Env:
         fused_rollout: the S steps of a replay as ONE launch with the state
         kept on chip between them (bitwise the same results) — None: where
         the scenario prefers it, True: wherever a rollout kernel exists
-        (simple_spread, transport / reverse_transport), False: never."""
+        (simple_spread, transport / reverse_transport, flocking), False: never."""
         return StepGraph(self, actions, steps_per_replay, validate, fused_rollout)
 
     @property

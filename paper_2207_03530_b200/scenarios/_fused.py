@@ -143,17 +143,20 @@ class FusedScenario(Scenario):
 
     def rollout_capable(self, world: World) -> bool:
         """A fused multi-step rollout kernel exists for this world
-        (ss_env_rollout: simple_spread, transport / reverse_transport with
-        their kernel's template, one physics step per Env.step)."""
-        return (self.native_id in (N.SCN_SIMPLE_SPREAD, N.SCN_TRANSPORT) and self.physics_fused(world)
+        (ss_env_rollout: simple_spread, transport / reverse_transport,
+        flocking with their kernel's template, one physics step per
+        Env.step)."""
+        return (self.native_id in (N.SCN_SIMPLE_SPREAD, N.SCN_TRANSPORT, N.SCN_FLOCKING) and self.physics_fused(world)
                 and world.params.substeps == 1 and len(world.agents) <= 8)
 
     def rollout_preferred(self, world: World) -> bool:
         """Take the rollout kernel by default (StepGraph fused_rollout=None)
-        wherever it exists: both steps are bound by their HBM traffic, which
-        the rollout cuts (measured at 1M envs: simple_spread 57.7 -> 36.6 us
-        per step, transport 80.2 -> 53.8)."""
-        return self.rollout_capable(world)
+        where the step is bound by the HBM traffic the rollout cuts:
+        simple_spread and transport (1M envs: 57.7 -> 36.6 us per step,
+        80.2 -> 53.8).  flocking's step is issue / latency bound (the lidar),
+        its rollout is within noise of the per-step graph (100k: 30.9 vs
+        31.3 us, 1M: 312 vs 296), so it stays opt-in."""
+        return self.native_id in (N.SCN_SIMPLE_SPREAD, N.SCN_TRANSPORT) and self.rollout_capable(world)
 
     def launch_rollout(self, world: World, step_action_ptrs: list, guard=None, stream: int | None = None,
                        check_actions: bool = False) -> list:

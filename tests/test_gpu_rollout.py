@@ -1,5 +1,5 @@
 """The fused rollout kernel (ss_env_rollout): S consecutive steps of
-simple_spread / transport / reverse_transport in ONE launch, each env's
+simple_spread / transport / reverse_transport / flocking in ONE launch, each env's
 state kept on chip between them.  Every intermediate StepResult, the final
 state and the step counters must equal eager Env.step bit for bit
 (env.py:209-235 per step), across the horizon, masked resets between
@@ -22,7 +22,9 @@ def outs(r):
 
 
 CASES = [("simple_spread", {}), ("simple_spread", {"n_agents": 1}), ("simple_spread", {"n_agents": 8}),
-         ("transport", {}), ("transport", {"n_agents": 7}), ("reverse_transport", {})]
+         ("transport", {}), ("transport", {"n_agents": 7}), ("reverse_transport", {}),
+         ("flocking", {}), ("flocking", {"n_agents": 3, "n_obstacles": 0}),
+         ("flocking", {"n_agents": 8, "n_obstacles": 6, "lidar_rays": 32})]
 
 
 @pytest.mark.parametrize("name,ov", CASES)
@@ -82,14 +84,15 @@ def test_rollout_nan_stops_mid_replay(cuda):
 
 def test_rollout_off_and_unsupported_fall_back_to_per_step(cuda):
     """fused_rollout=False, S=1, physics sub-steps, or a scenario without a
-    rollout kernel: the per-step graph; None (default) takes it wherever
-    one exists."""
+    rollout kernel: the per-step graph; None (default) takes it where the
+    scenario prefers it (simple_spread, transport; flocking is opt-in)."""
     B = 64
     for name, ov, S_, fused, want in [("simple_spread", {}, 4, False, False), ("simple_spread", {}, 1, True, False),
                                       ("simple_spread", {"substeps": 2}, 4, True, False),
-                                      ("flocking", {}, 4, True, False), ("transport", {}, 4, True, True),
+                                      ("dispersion", {}, 4, True, False), ("transport", {}, 4, True, True),
                                       ("transport", {}, 4, None, True), ("simple_spread", {}, 4, None, True),
-                                      ("flocking", {}, 4, None, False)]:
+                                      ("flocking", {}, 4, None, False), ("flocking", {}, 4, True, True),
+                                      ("discovery", {}, 4, None, False)]:
         e = S.Env(S.create_scenario(name), B, seed=1, device=cuda, validate=False, **ov)
         A = len(e.agents)
         buf = torch.zeros((A, B, 2), device=cuda)
