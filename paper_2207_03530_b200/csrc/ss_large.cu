@@ -39,6 +39,7 @@ struct LargeArgs {
   PhysK ph;
   const SsEntityDesc* ents;
   const float2* act[kLargeMaxAgents];
+  int64_t act_stride;   // act[k] == act[0] + k * act_stride for every agent (0: no such stride)
   float* obs;
   int64_t obs_stride;
   float* rew;
@@ -138,7 +139,11 @@ SS_DEV void agents_physics(const LargeArgs& a, float2* pos, float2* vel, int64_t
       ux[t] = 0.0f; uy[t] = 0.0f;
       if (k < a.NA) {
         const SsEntityDesc& d = a.ents[k];
-        const float2 u = a.act[k][e];
+        // one (A, B, 2) action tensor (the usual case): pointer arithmetic
+        // on act[0]; a per-lane index into the parameter table would
+        // serialise the constant cache over 32 addresses
+        const float2* ak = a.act_stride ? a.act[0] + k * a.act_stride : a.act[k];
+        const float2 u = ak[e];
         ux[t] = a.raw_forces ? u.x : fmul(clip_sym(u.x, d.u_range), d.u_mult);
         uy[t] = a.raw_forces ? u.y : fmul(clip_sym(u.y, d.u_range), d.u_mult);
         if (a.ph.has_gravity) { ux[t] = fadd(ux[t], d.grav_x); uy[t] = fadd(uy[t], d.grav_y); }
@@ -668,6 +673,9 @@ int launch_large(World& w, const SsBuffers* buf, const SsStepIO* io, cudaStream_
   }
   if (io->mode & SS_DO_PHYSICS) {
     for (int i = 0; i < a.NA; ++i) a.act[i] = reinterpret_cast<const float2*>(io->actions[i]);
+    a.act_stride = a.NA > 1 ? a.act[1] - a.act[0] : 0;
+    for (int i = 1; i < a.NA && a.act_stride != 0; ++i)
+      if (a.act[i] != a.act[0] + i * a.act_stride) a.act_stride = 0;
   }
   a.obs = io->obs;
   a.obs_stride = io->obs_agent_stride;
