@@ -462,6 +462,57 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_flocking(const
 #ifndef SS_FLOCK_WARPS
 #define SS_FLOCK_WARPS 40   // resident warps per SM the register budget is sized for
 #endif
+// Cold lidar paths of k_flocking_w, out of line (the fan screen is the hot
+// one): the per-ray screen when the fan is not uniform, and attached
+// rotations (sensors.py:121-135: per-ray fp64 angles).
+#ifndef SS_FLOCK_CONTACT
+#define SS_FLOCK_CONTACT contact_force_ol   // contact_force: inline at every call site
+#endif
+template <int NA>
+__device__ __noinline__ void flock_lidar_screened(int i, int lane, int NO, float4 me, const float2* spos,
+                                                  const float2* sst, const float2* sdir, const double2* sdird,
+                                                  RayScreen s_agent, RayScreen s_rock, double r2_agent,
+                                                  double r2_rock, int n_rays, float range_f, uint32_t* best) {
+  const double ox = (double)me.x, oy = (double)me.y;
+  for (int m = 0; m < n_rays; ++m) best[m] = 0x7f800000u;
+  for (int o = 0; o < NA; ++o) {
+    if (o == i) continue;
+    const float2 q = spos[o * 32 + lane];
+    const uint32_t mk = ray_mask(me.x - q.x, me.y - q.y, sdir, n_rays, s_agent);
+    ray_hits_f(mk, ox, oy, sdird, (double)q.x, (double)q.y, r2_agent, best, 1);
+  }
+  for (int r = 0; r < NO; ++r) {
+    const float2 q = sst[(1 + r) * 32 + lane];
+    const uint32_t mk = ray_mask(me.x - q.x, me.y - q.y, sdir, n_rays, s_rock);
+    ray_hits_f(mk, ox, oy, sdird, (double)q.x, (double)q.y, r2_rock, best, 1);
+  }
+  for (int m = 0; m < n_rays; ++m) best[m] = __float_as_uint(fminf(__uint_as_float(best[m]), range_f));
+}
+
+template <int NA>
+__device__ __noinline__ void flock_lidar_rotated(int i, int lane, int NO, float4 me, float rot_i,
+                                                 const float2* spos, const float2* sst, double r2_agent,
+                                                 double r2_rock, int n_rays, double ray_start, double ray_span,
+                                                 double lidar_range, float* out) {
+  const double ox = (double)me.x, oy = (double)me.y;
+  for (int m = 0; m < n_rays; ++m) {
+    const double ang = dadd_rn(dadd_rn(ray_start, (double)m * ray_span / n_rays), (double)rot_i);
+    double dx, dy;
+    sincos(ang, &dy, &dx);
+    double b = __longlong_as_double(0x7ff0000000000000LL);
+    for (int o = 0; o < NA; ++o) {
+      if (o == i) continue;
+      const float2 q = spos[o * 32 + lane];
+      b = fmin(b, ray_circle(ox, oy, dx, dy, (double)q.x, (double)q.y, r2_agent));
+    }
+    for (int r = 0; r < NO; ++r) {
+      const float2 q = sst[(1 + r) * 32 + lane];
+      b = fmin(b, ray_circle(ox, oy, dx, dy, (double)q.x, (double)q.y, r2_rock));
+    }
+    out[m] = (float)fmin(b, lidar_range);
+  }
+}
+
 // ROLL: the fused rollout (RolloutArgs *ro, SS_MODE_STEP): the steps of
 // the replay in one launch, the agents' rows kept in registers and the
 // beacon / rocks staged once; the per-step pointers come from ro.
@@ -539,11 +590,11 @@ SS_DEV void flocking_w_body(const SmallArgs& a, const FlockLidarK& lk, const Rol
       const float sign = ((i + j) & 1) ? -1.0f : 1.0f;
       float cx, cy;
       if (j < i) {
-        if (contact_force(q.x, q.y, me.x, me.y, dmin_aa, d2_aa, sign, a.ph.ck, a.ph.k, cx, cy)) {
+        if (SS_FLOCK_CONTACT(q.x, q.y, me.x, me.y, dmin_aa, d2_aa, sign, a.ph.ck, a.ph.k, cx, cy)) {
           fx = fsub(fx, cx); fy = fsub(fy, cy);
         }
       } else {
-        if (contact_force(me.x, me.y, q.x, q.y, dmin_aa, d2_aa, sign, a.ph.ck, a.ph.k, cx, cy)) {
+        if (SS_FLOCK_CONTACT(me.x, me.y, q.x, q.y, dmin_aa, d2_aa, sign, a.ph.ck, a.ph.k, cx, cy)) {
           fx = fadd(fx, cx); fy = fadd(fy, cy);
         }
       }
@@ -552,7 +603,7 @@ SS_DEV void flocking_w_body(const SmallArgs& a, const FlockLidarK& lk, const Rol
       const float2 q = sst[(1 + r) * 32 + lane];
       const float sign = ((i + NA + 1 + r) & 1) ? -1.0f : 1.0f;
       float cx, cy;
-      if (contact_force(me.x, me.y, q.x, q.y, dmin_ar, d2_ar, sign, a.ph.ck, a.ph.k, cx, cy)) {
+      if (SS_FLOCK_CONTACT(me.x, me.y, q.x, q.y, dmin_ar, d2_ar, sign, a.ph.ck, a.ph.k, cx, cy)) {
         fx = fadd(fx, cx); fy = fadd(fy, cy);
       }
     }
@@ -601,52 +652,22 @@ SS_DEV void flocking_w_body(const SmallArgs& a, const FlockLidarK& lk, const Rol
     }
     if (a.n_rays > 0) {
       const int c = 6 + 2 * NO + 2 * (NA - 1);
-      const double ox = (double)me.x, oy = (double)me.y;
       const float rot_i = (valid && a.attach_rot) ? a.s.rot[i * B + e].x : 0.0f;
       const bool fan = valid && rot_i == 0.0f;
       uint32_t* wbest = reinterpret_cast<uint32_t*>(srow + c);   // this warp's rows, lidar columns
       uint32_t* best = wbest + lane * P;
-      const int stride = 1;
       const float range_f = (float)a.lidar_range;
       if (lk.fan_ok) {
         // warp-collective: all lanes, including invalid / rotated ones
         lidar_fan_warp<NA>(fan, i, lane, NO, me.x, me.y, spos, sst, lk, sdird, wbest, P, squeue + i * kLidarQueue,
                            a.n_rays, __float_as_uint(range_f));
       } else if (fan) {
-        for (int m = 0; m < a.n_rays; ++m) best[m * stride] = 0x7f800000u;
-#pragma unroll
-        for (int o = 0; o < NA; ++o) {
-          if (o == i) continue;
-          const float2 q = spos[o * 32 + lane];
-          const uint32_t mk = ray_mask(me.x - q.x, me.y - q.y, sdir, a.n_rays, lk.agent);
-          ray_hits_f(mk, ox, oy, sdird, (double)q.x, (double)q.y, lk.r2_agent, best, stride);
-        }
-        for (int r = 0; r < NO; ++r) {
-          const float2 q = sst[(1 + r) * 32 + lane];
-          const uint32_t mk = ray_mask(me.x - q.x, me.y - q.y, sdir, a.n_rays, lk.rock);
-          ray_hits_f(mk, ox, oy, sdird, (double)q.x, (double)q.y, lk.r2_rock, best, stride);
-        }
-        for (int m = 0; m < a.n_rays; ++m) best[m] = __float_as_uint(fminf(__uint_as_float(best[m]), range_f));
+        flock_lidar_screened<NA>(i, lane, NO, me, spos, sst, sdir, sdird, lk.agent, lk.rock, lk.r2_agent,
+                                 lk.r2_rock, a.n_rays, range_f, best);
       }
-      if (valid && !fan) {
-        // attached rotation (sensors.py:121-135): per-ray fp64 angles
-        for (int m = 0; m < a.n_rays; ++m) {
-          const double ang = dadd_rn(dadd_rn(a.ray_start, (double)m * a.ray_span / a.n_rays), (double)rot_i);
-          double dx, dy;
-          sincos(ang, &dy, &dx);
-          double b = __longlong_as_double(0x7ff0000000000000LL);
-          for (int o = 0; o < NA; ++o) {
-            if (o == i) continue;
-            const float2 q = spos[o * 32 + lane];
-            b = fmin(b, ray_circle(ox, oy, dx, dy, (double)q.x, (double)q.y, lk.r2_agent));
-          }
-          for (int r = 0; r < NO; ++r) {
-            const float2 q = sst[(1 + r) * 32 + lane];
-            b = fmin(b, ray_circle(ox, oy, dx, dy, (double)q.x, (double)q.y, lk.r2_rock));
-          }
-          row[c + m] = (float)fmin(b, a.lidar_range);
-        }
-      }
+      if (valid && !fan)
+        flock_lidar_rotated<NA>(i, lane, NO, me, rot_i, spos, sst, lk.r2_agent, lk.r2_rock, a.n_rays,
+                                a.ray_start, a.ray_span, a.lidar_range, row + c);
     }
     if (nvalid > 0) warp_flush_padded(obs_out + i * a.obs_stride + e0 * O, nvalid, O, P, srow);
   }

@@ -191,6 +191,33 @@ SS_DEV bool contact_force(float pix, float piy, float pjx, float pjy, float dmin
   return true;
 }
 
+// The active-pair part of contact_force (square root, the two divisions,
+// the softplus) as ONE out-of-line copy: kernels that would otherwise inline
+// it at many call sites (k_flocking_w) keep their hot loop in the
+// instruction cache.  Returns the force on i; same arithmetic as above.
+static __device__ __noinline__ float2 contact_active(float x, float y, float d2, float dmin, float sign, float ck,
+                                              float k) {
+  const float d = fsqrt(d2);
+  float dx, dy;
+  if (d < 1e-8f) { dx = sign; dy = 0.0f; }            // DEGENERATE_DIST, dynamics.py:23
+  else { dx = fdiv(x, d); dy = fdiv(y, d); }
+  const float mag = fmul(ck, np_softplus(fdiv(fsub(dmin, d), k)));
+  return make_float2(fmul(dx, mag), fmul(dy, mag));
+}
+
+// contact_force with the active part out of line.
+SS_DEV bool contact_force_ol(float pix, float piy, float pjx, float pjy, float dmin, float d2_act,
+                             float sign, float ck, float k, float& fx, float& fy) {
+  const float x = fsub(pix, pjx);
+  const float y = fsub(piy, pjy);
+  const float d2 = fadd(fmul(x, x), fmul(y, y));
+  if (!(d2 <= d2_act)) { fx = 0.0f; fy = 0.0f; return false; }
+  const float2 f = contact_active(x, y, d2, dmin, sign, ck, k);
+  fx = f.x;
+  fy = f.y;
+  return true;
+}
+
 // closest_point_on_box (geometry.py:79-100): numpy promotes the wall
 // selection to float64 (np.where over two Python floats), so the world-frame
 // point is evaluated in double and rounded once when Vec2 casts to float32.

@@ -40,6 +40,10 @@ def main() -> None:
         for row in raw[2:]:
             name = row[hdr.index("Kernel Name")] if "Kernel Name" in hdr else "kernel"
             m = {k: (row[hdr.index(k)], units[hdr.index(k)]) for k in KEYS if k in hdr}
+            # warp-stall reasons (cycles per issued instruction, by reason)
+            for j, k in enumerate(hdr):
+                if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio"):
+                    m[k] = (row[j], units[j])
             out[name] = m
     json.dump(out, open(prefix + ".metrics.json", "w"), indent=1)
     src = ncu("-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass")
