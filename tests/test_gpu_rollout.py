@@ -100,3 +100,24 @@ def test_rollout_off_and_unsupported_fall_back_to_per_step(cuda):
         assert graph.fused_rollout is want, name
         assert graph.launches_per_replay == (1 if want else S_)
         graph.step()
+
+
+@pytest.mark.parametrize("name", ["transport", "reverse_transport"])
+def test_rollout_one_wave_build_equals_eager(cuda, name):
+    """100k envs: 782 CTAs, so the launcher takes the 80-register transport
+    rollout build (one wave) instead of the 96-register one; same results."""
+    B, S_ = 100_000, 4
+    a = S.Env(S.create_scenario(name), B, seed=8, device=cuda, validate=False, max_steps=3)
+    b = S.Env(S.create_scenario(name), B, seed=8, device=cuda, validate=False, max_steps=3)
+    A = len(a.agents)
+    g = torch.Generator(device=cuda)
+    g.manual_seed(4)
+    bufs = [torch.rand((A, B, 2), device=cuda, generator=g) * 2 - 1 for _ in range(2)]
+    graph = b.step_graph(bufs, steps_per_replay=S_, fused_rollout=True)
+    for rep in range(2):
+        rs = graph.rollout(rep % 2)
+        for s in range(S_):
+            ra = a.step(bufs[(rep + s) % 2])
+            for x, y in zip(outs(ra), outs(rs[s])):
+                assert torch.equal(x, y), f"replay {rep} step {s}"
+    np.testing.assert_array_equal(state(a), state(b))
