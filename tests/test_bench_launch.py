@@ -51,3 +51,16 @@ def test_cpu_rate_uses_reference_when_installed():
     r = bench.cpu_rate("simple_spread", 64, 2)
     assert r["kind"] == ("reference" if bench.load_reference() is not None else "port")
     assert r["agent_steps_per_s"] > 0
+
+
+def test_byte_model_per_step_and_rollout():
+    """bench.step_bytes: a per-step launch moves everything once (DESIGN.md §4
+    table); a rollout of S steps pays the state / static / step_count part
+    once per S steps."""
+    want = {"simple_spread": (3, 3, 14, 341), "transport": (4, 2, 12, 433), "flocking": (5, 4, 32, 917)}
+    for scen, (A, n_other, O, total) in want.items():
+        per_step, per_launch = bench.step_bytes(scen, A, n_other, O)
+        assert per_step + per_launch == total == bench.bytes_per_env_step(scen, A, n_other, O)
+        assert bench.bytes_per_env_step(scen, A, n_other, O, 10) == per_step + per_launch / 10
+    assert bench.bytes_per_env_step("dispersion", 64, 64, 196) == 53533
+    assert bench.bytes_per_env_step("discovery", 64, 3, 136) == 37705
