@@ -46,7 +46,7 @@ __device__ __noinline__ void catalog_physics(const SmallArgs& a, int NA, int n_s
 // float32 cos/sin.  sc[0] = f32(target_spin).
 // ---------------------------------------------------------------------------
 template <int NA>
-__global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_wheel(const SmallArgs a) {
+__global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_wheel(const __grid_constant__ SmallArgs a) {
   extern __shared__ __align__(16) float smem[];
   grid_dep_sync();
   if (guard_tripped(a.guard, a.guard_n)) return;
@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_wheel(const Sm
 // vel, f32(alcove_x - float64(x)), f32(alcove_y - float64(y))].
 // sc[0] = f32(0.15); sd[0], sd[1] = alcove (python doubles).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_give_way(const SmallArgs a) {
+__global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_give_way(const __grid_constant__ SmallArgs a) {
   extern __shared__ __align__(16) float smem[];
   grid_dep_sync();
   if (guard_tripped(a.guard, a.guard_n)) return;
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_give_way(const
 // sc[2] = f32(0.05); sd[0], sd[1] = gap centres (python doubles).
 // ---------------------------------------------------------------------------
 template <int NA>
-__global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_passage(const SmallArgs a) {
+__global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_passage(const __grid_constant__ SmallArgs a) {
   extern __shared__ __align__(16) float smem[];
   grid_dep_sync();
   if (guard_tripped(a.guard, a.guard_n)) return;
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_passage(const 
 // sc[0] = f32 drop height, sc[1] = f32(0.08).
 // ---------------------------------------------------------------------------
 template <int NA>
-__global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_balance(const SmallArgs a) {
+__global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_balance(const __grid_constant__ SmallArgs a) {
   extern __shared__ __align__(16) float smem[];
   grid_dep_sync();
   if (guard_tripped(a.guard, a.guard_n)) return;
@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_balance(const 
 constexpr int kWaterfallMaxBlocks = 8;
 
 template <int NA>
-__global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_waterfall(const SmallArgs a) {
+__global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_waterfall(const __grid_constant__ SmallArgs a) {
   extern __shared__ __align__(16) float smem[];
   grid_dep_sync();
   if (guard_tripped(a.guard, a.guard_n)) return;
@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_waterfall(cons
 // f32(0.1), sc[2] = f32(hx); sd[0] = hx (python double).
 // ---------------------------------------------------------------------------
 template <int NA>
-__global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_football(const SmallArgs a) {
+__global__ void __launch_bounds__(kSmallThreads, SS_SMALL_MINB) k_football(const __grid_constant__ SmallArgs a) {
   extern __shared__ __align__(16) float smem[];
   grid_dep_sync();
   if (guard_tripped(a.guard, a.guard_n)) return;
