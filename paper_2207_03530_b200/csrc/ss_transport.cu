@@ -43,7 +43,7 @@ SS_DEV void transport_physics(float (&px)[NA + 1], float (&py)[NA + 1], float (&
   float fx[NA + 1], fy[NA + 1];
 #pragma unroll
   for (int i = 0; i < NA; ++i) {
-    const SsEntityDesc& d = a.ents[i];
+    const SsEntityDesc& d = tmpl_ent(a, i);
     fx[i] = decode_axis(act[i].x, d, a.raw_forces);
     fy[i] = decode_axis(act[i].y, d, a.raw_forces);
   }
@@ -51,7 +51,7 @@ SS_DEV void transport_physics(float (&px)[NA + 1], float (&py)[NA + 1], float (&
   if (a.ph.has_gravity) {
 #pragma unroll
     for (int i = 0; i <= NA; ++i) {
-      fx[i] = fadd(fx[i], a.ents[i].grav_x); fy[i] = fadd(fy[i], a.ents[i].grav_y);
+      fx[i] = fadd(fx[i], tmpl_ent(a, i).grav_x); fy[i] = fadd(fy[i], tmpl_ent(a, i).grav_y);
     }
   }
   // (1) geometry + activity, pair order
@@ -63,7 +63,7 @@ SS_DEV void transport_physics(float (&px)[NA + 1], float (&py)[NA + 1], float (&
 #pragma unroll
       for (int j = i + 1; j < NA; ++j, ++p) {
         const float x = fsub(px[i], px[j]), y = fsub(py[i], py[j]);
-        if (fadd(fmul(x, x), fmul(y, y)) <= a.pairs[p].d2_act) {
+        if (fadd(fmul(x, x), fmul(y, y)) <= tmpl_pair(a, p).d2_act) {
           act_mask |= 1ull << p;
           scr[p * 32] = make_float2(x, y);
         }
@@ -71,7 +71,7 @@ SS_DEV void transport_physics(float (&px)[NA + 1], float (&py)[NA + 1], float (&
       float qx, qy;   // agent i vs package (sphere-box): closest point on the box
       closest_point_on_box(px[i], py[i], px[NA], py[NA], ca, sa, hx, hy, qx, qy);
       const float x = fsub(px[i], qx), y = fsub(py[i], qy);
-      if (fadd(fmul(x, x), fmul(y, y)) <= a.pairs[p].d2_act) {
+      if (fadd(fmul(x, x), fmul(y, y)) <= tmpl_pair(a, p).d2_act) {
         act_mask |= 1ull << p;
         scr[p * 32] = make_float2(x, y);
       }
@@ -107,7 +107,7 @@ SS_DEV void transport_physics(float (&px)[NA + 1], float (&py)[NA + 1], float (&
   }
 #pragma unroll
   for (int i = 0; i <= NA; ++i) {
-    const SsEntityDesc& d = a.ents[i];
+    const SsEntityDesc& d = tmpl_ent(a, i);
     integrate_lin(px[i], py[i], vx[i], vy[i], fx[i], fy[i], a.ph.keep, d.inv_m_dt, a.ph.dt,
                   d.max_speed);
     // single step: store each row as soon as it is final (the LSU drains
