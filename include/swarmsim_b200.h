@@ -288,6 +288,13 @@ int ss_mask_count(void* world, const uint8_t* mask, int64_t* count_out, void* st
  * (device int32) to nonzero when any value is NaN.  Does not clear it. */
 int ss_check_actions(void* world, const float* const* actions, int32_t* flag_out, void* stream);
 
+/* Publish the NaN verdict to the host (extension): host_out[i] = flag[i]
+ * for i < n, stored by a one-CTA kernel into host-mapped pinned memory
+ * (cudaHostAlloc; unified addressing), so the caller waits on an event
+ * instead of a device-to-host copy that would queue behind observation
+ * copies in flight on the copy engine (Env.step(validate=True)). */
+int ss_publish_flag(const int32_t* flag, int32_t* host_out, int32_t n, void* stream);
+
 /* lidar_scan (sensors.py:138-146) for one agent: out[B][n_rays] f32. */
 int ss_lidar(void* world, const SsBuffers* buf, int32_t agent, const SsLidarDesc* lidar,
              float* out, void* stream);

@@ -32,6 +32,7 @@ int launch_reset(World& w, const SsBuffers* buf, const uint8_t* mask, const int6
 int launch_mask_count(World& w, const uint8_t* mask, int64_t* count_out, cudaStream_t st);
 int launch_check_actions(int n_agents, int64_t B, const float* const* actions, int* flag,
                          cudaStream_t st);
+int launch_publish_flag(const int* flag, int* host_out, int n, cudaStream_t st);
 int launch_collision_force(const float* pix, const float* piy, const float* pjx, const float* pjy,
                            float dmin, float sign, float ck, float k, float* fx, float* fy,
                            uint8_t* active, int64_t n, cudaStream_t st);
@@ -247,6 +248,11 @@ int ss_check_actions(void* world, const float* const* actions, int32_t* flag_out
   if (!w || !flag_out) { set_error("null argument"); return SS_ERR_CONTRACT; }
   return launch_check_actions(w->d.n_agents, w->d.batch, actions, flag_out,
                               static_cast<cudaStream_t>(stream));
+}
+
+int ss_publish_flag(const int32_t* flag, int32_t* host_out, int32_t n, void* stream) {
+  if (!flag || !host_out || n < 1 || n > 1024) { set_error("publish_flag: 1..1024 words"); return SS_ERR_CONTRACT; }
+  return launch_publish_flag(flag, host_out, n, static_cast<cudaStream_t>(stream));
 }
 
 int ss_lidar(void* world, const SsBuffers* buf, int32_t agent, const SsLidarDesc* lidar,

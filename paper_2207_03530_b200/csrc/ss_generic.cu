@@ -217,6 +217,18 @@ int launch_check_actions(int n_agents, int64_t B, const float* const* actions, i
   return cuda_status(cudaGetLastError(), "action check launch");
 }
 
+// Copy the verdict words into host-mapped memory with plain stores (PCIe
+// posted writes; no copy engine).
+__global__ void k_publish_flag(const int* flag, int* host_out, int n) {
+  grid_dep_sync();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) host_out[i] = flag[i];
+}
+
+int launch_publish_flag(const int* flag, int* host_out, int n, cudaStream_t st) {
+  launch_step(k_publish_flag, dim3(1), dim3(32), 0, st, flag, host_out, n);
+  return cuda_status(cudaGetLastError(), "publish_flag launch");
+}
+
 int launch_collision_force(const float* pix, const float* piy, const float* pjx, const float* pjy,
                            float dmin, float sign, float ck, float k, float* fx, float* fy,
                            uint8_t* active, int64_t n, cudaStream_t st) {

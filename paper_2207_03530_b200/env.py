@@ -192,6 +192,12 @@ class Env:
         self.action_specs = [ActionSpec(mode=action_mode, comm_dim=0 if a.silent else a.comm_dim)
                              for a in self.world.agents]
         self._flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        # the verdict's host copy: pinned, device-mapped (unified addressing),
+        # written by a kernel store (ss_publish_flag) and read after an event
+        # wait — a device-to-host copy would queue behind any observation
+        # copies in flight on the copy engine
+        self._flag_host = torch.zeros(1, dtype=torch.int32).pin_memory()
+        self._flag_event = torch.cuda.Event()
         self.reset()
 
     # -- properties ----------------------------------------------------------
@@ -360,7 +366,7 @@ class Env:
             guard = self._flag
         obs, rew, done = sc.launch(world, N.MODE_STEP, action_ptrs=ptrs, raw_forces=raw, guard=guard,
                                    flip_rng=False, stream=st)
-        if guard is not None and int(self._flag.item()) != 0:
+        if guard is not None and self._verdict(st) != 0:
             forces = keepalive if isinstance(keepalive, list) else list(keepalive.unbind(0))
             bad = next(a.name for a, f in zip(self.agents, forces) if f is not None and bool(torch.isnan(f).any()))
             raise ContractViolation(f"action for '{bad}' contains NaN")
@@ -375,6 +381,14 @@ class Env:
         else:
             infos = [sc.info(a, world) for a in self.agents]
         return StepResult(obs=obs_list, rewards=list(rew.unbind(0)), dones=done, infos=infos)
+
+    def _verdict(self, st: int) -> int:
+        """The NaN verdict of the step just queued on stream `st` (host sync
+        on that stream's work only)."""
+        N.check(N.lib().ss_publish_flag(self._flag.data_ptr(), self._flag_host.data_ptr(), 1, st))
+        self._flag_event.record(torch.cuda.current_stream(self.device))
+        self._flag_event.synchronize()
+        return int(self._flag_host[0])
 
     def _capture_step(self, ptrs, keepalive, flags=None, n_flags: int = 1) -> StepResult:
         """One fused step without host syncs (graph capture).  flags: device
