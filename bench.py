@@ -74,11 +74,12 @@ def bytes_per_env_step(scenario: str, A: int, n_other: int, obs_dim: int, steps_
 # name: scenario, overrides, envs (per GPU, or global with --strong),
 # (1-core cpu_baseline sample envs, steps), reference-arm sample envs per step
 WORKLOADS = {
-    "simple_spread": ("simple_spread", {"n_agents": 3}, 1_000_000, (1_000_000, 5), 1_000_000),
-    "transport": ("transport", {"n_agents": 4}, 100_000, (100_000, 10), 100_000),
-    "flocking": ("flocking", {"n_agents": 5, "n_obstacles": 3, "lidar_rays": 12}, 100_000, (20_000, 5), 100_000),
-    "dispersion": ("dispersion", {"n_agents": 64, "n_food": 64}, 262_144, (1024, 3), 8192),
-    "discovery": ("discovery", {"n_agents": 64}, 262_144, (2048, 3), 32768),
+    # cpu_baseline samples (envs, steps): ~10 s of one host core each
+    "simple_spread": ("simple_spread", {"n_agents": 3}, 1_000_000, (1_000_000, 20), 1_000_000),
+    "transport": ("transport", {"n_agents": 4}, 100_000, (100_000, 200), 100_000),
+    "flocking": ("flocking", {"n_agents": 5, "n_obstacles": 3, "lidar_rays": 12}, 100_000, (20_000, 50), 100_000),
+    "dispersion": ("dispersion", {"n_agents": 64, "n_food": 64}, 262_144, (1024, 7), 8192),
+    "discovery": ("discovery", {"n_agents": 64}, 262_144, (2048, 25), 32768),
 }
 
 
