@@ -186,6 +186,9 @@ constexpr int kLidarQueue = 128;   // (lane, target, ray) tests staged per warp 
 // the non-negative float pattern): float(min(t, range)) == min(float(t),
 // float(range)) since rounding is monotone, so the scan stays bit-identical.
 // Warp-collective: every lane of the warp must call it.
+#ifndef SS_LIDAR_ROLLED
+#define SS_LIDAR_ROLLED 0
+#endif
 template <int NA>
 SS_DEV void lidar_fan_warp(bool active, int i, int lane, int NO, float mex, float mey,
                            const float2* spos, const float2* sst, const FlockLidarK& lk,
@@ -194,7 +197,13 @@ SS_DEV void lidar_fan_warp(bool active, int i, int lane, int NO, float mex, floa
   constexpr int NT = NA - 1 + kFlockMaxRocks;
   uint32_t mk[NT];
   int cnt = 0;
+  // SS_LIDAR_ROLLED: the per-target loops rolled (one copy of the screen
+  // code; the masks then live in local memory) to shrink the hot code
+#if SS_LIDAR_ROLLED
+#pragma unroll 1
+#else
 #pragma unroll
+#endif
   for (int t = 0; t < NT; ++t) {
     mk[t] = 0u;
     if (active && (t < NA - 1 || t - (NA - 1) < NO)) {
@@ -224,7 +233,11 @@ SS_DEV void lidar_fan_warp(bool active, int i, int lane, int NO, float mex, floa
   for (int base = 0; base < total; base += kLidarQueue) {
     if (excl < base + kLidarQueue && excl + cnt > base) {
       int idx = excl;
+#if SS_LIDAR_ROLLED
+#pragma unroll 1
+#else
 #pragma unroll
+#endif
       for (int t = 0; t < NT; ++t) {
         uint32_t m = mk[t];
         while (m) {
