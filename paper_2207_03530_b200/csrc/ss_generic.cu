@@ -153,19 +153,22 @@ struct CheckArgs {
   int* flag;
 };
 
-// NaN scan of every agent's action block (env.py:85): one grid-stride pass
-// over all agents' floats (16-byte loads when aligned), the verdict ORed into
-// *flag.  Sized to the SM count, not to the agent count.
+// NaN scan of every agent's action block (env.py:85): blockIdx.y = agent,
+// a grid-stride pass over that agent's floats along x (16-byte loads when
+// aligned, four in flight per thread), the verdict ORed into *flag.  About
+// 4 CTAs per SM over all the agents together: with A = 64 agents a 1-D grid
+// over the agents in turn left each thread ~1 load per agent, 64 dependent
+// rounds of memory latency.
 __global__ void __launch_bounds__(512) k_check_actions(const CheckArgs a) {
   grid_dep_sync();
   bool bad = false;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
   if (a.vec4) {
     const int64_t n4 = a.n >> 2;
-    for (int i = 0; i < a.A; ++i) {
-      const float4* p = reinterpret_cast<const float4*>(a.act[i]);
-      if (p == nullptr) continue;           // a script drives this agent (no raw action)
+    const float4* p = reinterpret_cast<const float4*>(a.act[i]);
+    if (p != nullptr) {                     // nullptr: a script drives this agent (no raw action)
       int64_t k = t0;
       for (; k + 3 * stride < n4; k += 4 * stride) {   // four 16-byte loads in flight
         float4 v[4];
@@ -180,11 +183,9 @@ __global__ void __launch_bounds__(512) k_check_actions(const CheckArgs a) {
       }
     }
   } else {
-    for (int i = 0; i < a.A; ++i) {
-      const float* p = a.act[i];
-      if (p == nullptr) continue;
+    const float* p = a.act[i];
+    if (p != nullptr)
       for (int64_t k = t0; k < a.n; k += stride) bad |= isnan(p[k]);
-    }
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(a.flag, 1);
 }
@@ -211,9 +212,10 @@ int launch_check_actions(int n_agents, int64_t B, const float* const* actions, i
     if (sms <= 0) sms = 148;
   }
   const int64_t per_block = 512LL * (a.vec4 ? 4 : 1);
-  const int64_t want = (a.n + per_block - 1) / per_block;
-  const unsigned grid = (unsigned)(want < 4LL * sms ? (want > 0 ? want : 1) : 4LL * sms);
-  launch_step(k_check_actions, dim3(grid), dim3(512), 0, st, a);
+  const int64_t want = (a.n + per_block - 1) / per_block;   // CTAs one agent's block could use
+  const int64_t cap = (4LL * sms + n_agents - 1) / n_agents;  // ~4 CTAs per SM over all agents
+  const unsigned gx = (unsigned)std::max<int64_t>(1, std::min(want, cap));
+  launch_step(k_check_actions, dim3(gx, n_agents), dim3(512), 0, st, a);
   return cuda_status(cudaGetLastError(), "action check launch");
 }
 
