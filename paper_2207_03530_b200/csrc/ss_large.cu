@@ -287,11 +287,27 @@ struct ChunkWalk {
 // ---------------------------------------------------------------------------
 // discovery (scenarios/discovery.py)
 // ---------------------------------------------------------------------------
-// 16-byte chunk c of discovery observation row r (see k_discovery).
-SS_DEV float4 disc_chunk(const float2* t2, const WarpSmem& sm, int first_agent_slot, int r, int c) {
+// 16-byte chunk c of discovery observation row r (see k_discovery).  With
+// SS_DISC_SHIFT the template also exists shifted by one slot (t1[s] =
+// t2[s + 1]), so the chunk's two slots are one 16-byte load from t2 (both
+// before the row's own agent) or t1 (both after it); only the chunk that
+// straddles the skipped slot takes a second load.
+#ifndef SS_DISC_SHIFT
+#define SS_DISC_SHIFT 1
+#endif
+SS_DEV float4 disc_chunk(const float2* t2, const float2* t1, const WarpSmem& sm, int first_agent_slot, int r,
+                         int c) {
   const int skip = first_agent_slot + r;
   const int s0 = 2 * c, s1 = s0 + 1;
-  const float2 q0 = t2[s0 + (s0 >= skip)], q1 = t2[s1 + (s1 >= skip)];
+  float2 q0, q1;
+  if (SS_DISC_SHIFT) {
+    const float4 q = reinterpret_cast<const float4*>(s0 >= skip ? t1 : t2)[c];
+    q0 = make_float2(q.x, q.y);
+    q1 = s1 == skip ? t1[s1] : make_float2(q.z, q.w);
+  } else {
+    q0 = t2[s0 + (s0 >= skip)];
+    q1 = t2[s1 + (s1 >= skip)];
+  }
   const float2 pk = sm.pos[r];
   if (c == 0) {
     const float2 vk = sm.vel[r];
@@ -413,6 +429,13 @@ __global__ void __launch_bounds__(32 * kLargeWarps, SS_LARGE_MINB) k_discovery(c
     // slot s + 1 beyond it.
     const float2* t2 = reinterpret_cast<const float2*>(sm.tmpl);
     const int first_agent_slot = 2 + a.NL;
+    // the one-slot-shifted template, in the contact bitmap's region (free
+    // after the physics)
+    float2* t1 = reinterpret_cast<float2*>(sm.tmpl_shift);
+    if (SS_DISC_SHIFT) {
+      for (int k = lane; k < 1 + a.NL + a.NA; k += 32) t1[k] = t2[k + 1];
+      __syncwarp();
+    }
     if (VEC == 4) {
       // all rows' 16-byte chunks as one flattened run, lane l taking l,
       // l+32, ...; slot s of row k reads template slot s + (s >= 2+NL+k)
@@ -431,7 +454,7 @@ __global__ void __launch_bounds__(32 * kLargeWarps, SS_LARGE_MINB) k_discovery(c
           float4* dst[kObsUnroll];
 #pragma unroll
           for (int u = 0; u < kObsUnroll; ++u) {
-            v[u] = disc_chunk(t2, sm, first_agent_slot, r, c);
+            v[u] = disc_chunk(t2, t1, sm, first_agent_slot, r, c);
             dst[u] = rowp + c;
             c += 32;
             if (c >= nch) { c -= nch; ++r; rowp += stride4; }
@@ -440,7 +463,7 @@ __global__ void __launch_bounds__(32 * kLargeWarps, SS_LARGE_MINB) k_discovery(c
           for (int u = 0; u < kObsUnroll; ++u) __stcs(dst[u], v[u]);
         }
         for (; idx < total; idx += 32) {
-          __stcs(rowp + c, disc_chunk(t2, sm, first_agent_slot, r, c));
+          __stcs(rowp + c, disc_chunk(t2, t1, sm, first_agent_slot, r, c));
           c += 32;
           if (c >= nch) { c -= nch; ++r; rowp += stride4; }
         }
@@ -448,7 +471,7 @@ __global__ void __launch_bounds__(32 * kLargeWarps, SS_LARGE_MINB) k_discovery(c
         for (int idx = lane; idx < total; idx += 32) {
           const int r = idx / nch, c = idx - r * nch;
           __stcs(reinterpret_cast<float4*>(a.obs + r * a.obs_stride + e * a.O) + c,
-                 disc_chunk(t2, sm, first_agent_slot, r, c));
+                 disc_chunk(t2, t1, sm, first_agent_slot, r, c));
         }
       }
     } else {
