@@ -121,3 +121,26 @@ def test_rollout_one_wave_build_equals_eager(cuda, name):
             for x, y in zip(outs(ra), outs(rs[s])):
                 assert torch.equal(x, y), f"replay {rep} step {s}"
     np.testing.assert_array_equal(state(a), state(b))
+
+
+@pytest.mark.parametrize("B", [1, 31, 33])
+@pytest.mark.parametrize("name", ["simple_spread", "transport", "flocking"])
+def test_rollout_ragged_batches(cuda, name, B):
+    """Partial warps (B < 32, B = 33: the last warp's observation rows take
+    the plain store path instead of the bulk copy) and S above the rollout
+    limit (17 > 16: per-step graph) still equal eager stepping."""
+    for S_, fused in ((3, True), (17, None)):
+        a = S.Env(S.create_scenario(name), B, seed=9, device=cuda, validate=False)
+        b = S.Env(S.create_scenario(name), B, seed=9, device=cuda, validate=False)
+        A = len(a.agents)
+        g = torch.Generator(device=cuda)
+        g.manual_seed(13)
+        bufs = [torch.rand((A, B, 2), device=cuda, generator=g) * 2 - 1 for _ in range(2)]
+        graph = b.step_graph(bufs, steps_per_replay=S_, fused_rollout=fused)
+        assert graph.fused_rollout is (S_ <= 16)
+        rs = graph.rollout(0)
+        for s in range(S_):
+            ra = a.step(bufs[s % 2])
+            for x, y in zip(outs(ra), outs(rs[s])):
+                assert torch.equal(x, y), f"{name} B={B} S={S_} step {s}"
+        np.testing.assert_array_equal(state(a), state(b))
