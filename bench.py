@@ -623,7 +623,7 @@ def run_b200(args, rank, world, local) -> None:
                     "d2h_frac_of_pinned": d2h * E2E_K / e2e_sec / 1e9 / link["d2h"],
                     "obs_on_device": {"value": Bg * A * E2E_K / metric_sec, "h2d_bytes_per_step": h2d,
                                       "d2h_bytes_per_step": A * B * 4 + B}},
-            # per replay: the S action scans + the S step kernels or one rollout kernel
+            # per replay: one action-scan launch (per 16 steps) + the S step kernels or one rollout kernel
             "gpu_launches": R * launches_per_replay,
             "fused_rollout": graph_fused,
             "steps_per_replay": S,

@@ -288,6 +288,14 @@ int ss_mask_count(void* world, const uint8_t* mask, int64_t* count_out, void* st
  * (device int32) to nonzero when any value is NaN.  Does not clear it. */
 int ss_check_actions(void* world, const float* const* actions, int32_t* flag_out, void* stream);
 
+/* NaN scans of n_sets action sets in ONE launch (extension; a replay of
+ * n_sets steps): set s holds n_agents blocks of n_floats f32, agent_stride
+ * floats apart, from device pointer bases[s] (HOST array).  Zeroes
+ * flags[0 .. n_sets) and sets flags[s] nonzero when set s holds a NaN
+ * (env.py:85 per step).  1 <= n_sets <= SS_MAX_ROLLOUT. */
+int ss_check_action_sets(const float* const* bases, int32_t n_sets, int32_t n_agents, int64_t agent_stride,
+                         int64_t n_floats, int32_t* flags, void* stream);
+
 /* Publish the NaN verdict to the host (extension): host_out[i] = flag[i]
  * for i < n, stored by a one-CTA kernel into host-mapped pinned memory
  * (cudaHostAlloc; unified addressing), so the caller waits on an event

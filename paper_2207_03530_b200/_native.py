@@ -118,6 +118,7 @@ def _declare(lib) -> None:
     lib.ss_mask_count.argtypes = [c_vp, c_vp, c_vp, c_vp]
     lib.ss_check_actions.argtypes = [c_vp, P(c_vp), c_vp, c_vp]
     lib.ss_publish_flag.argtypes = [c_vp, c_vp, c_i32, c_vp]
+    lib.ss_check_action_sets.argtypes = [P(c_vp), c_i32, c_i32, c_i64, c_i64, c_vp, c_vp]
     lib.ss_lidar.argtypes = [c_vp, P(SsBuffers), c_i32, P(SsLidarDesc), c_vp, c_vp]
     lib.ss_cast_ray.argtypes = [c_vp, P(SsBuffers), c_i32, c_vp, c_vp, c_vp, c_f64, c_vp, c_vp]
     lib.ss_np_trig.argtypes = [c_vp, c_vp, c_i64, c_i32, c_vp]
@@ -126,7 +127,7 @@ def _declare(lib) -> None:
     lib.ss_closest_points.argtypes = [c_vp, c_vp, c_i32, c_f64, c_f64, c_vp, c_vp, c_i32,
                                       c_f64, c_f64, c_vp, c_vp, c_i64, c_vp, c_vp]
     for name in ("ss_world_create", "ss_world_destroy", "ss_env_step", "ss_env_rollout", "ss_world_step", "ss_reset",
-                 "ss_mask_count", "ss_check_actions", "ss_publish_flag", "ss_lidar", "ss_cast_ray",
+                 "ss_mask_count", "ss_check_actions", "ss_check_action_sets", "ss_publish_flag", "ss_lidar", "ss_cast_ray",
                  "ss_collision_force", "ss_closest_points", "ss_np_trig"):
         getattr(lib, name).restype = c_i32
 
@@ -151,7 +152,8 @@ def lib():
 def exported_symbols() -> list[str]:
     return [
         "ss_abi_version", "ss_last_error", "ss_world_create", "ss_world_destroy", "ss_env_step", "ss_env_rollout",
-        "ss_world_step", "ss_reset", "ss_mask_count", "ss_check_actions", "ss_publish_flag", "ss_lidar",
+        "ss_world_step", "ss_reset", "ss_mask_count", "ss_check_actions", "ss_check_action_sets",
+        "ss_publish_flag", "ss_lidar",
         "ss_cast_ray", "ss_collision_force", "ss_closest_points", "ss_np_trig",
     ]
 

@@ -33,6 +33,8 @@ int launch_mask_count(World& w, const uint8_t* mask, int64_t* count_out, cudaStr
 int launch_check_actions(int n_agents, int64_t B, const float* const* actions, int* flag,
                          cudaStream_t st);
 int launch_publish_flag(const int* flag, int* host_out, int n, cudaStream_t st);
+int launch_check_sets(const float* const* bases, int n_sets, int A, int64_t agent_stride, int64_t n,
+                      int* flags, cudaStream_t st);
 int launch_collision_force(const float* pix, const float* piy, const float* pjx, const float* pjy,
                            float dmin, float sign, float ck, float k, float* fx, float* fy,
                            uint8_t* active, int64_t n, cudaStream_t st);
@@ -248,6 +250,21 @@ int ss_check_actions(void* world, const float* const* actions, int32_t* flag_out
   if (!w || !flag_out) { set_error("null argument"); return SS_ERR_CONTRACT; }
   return launch_check_actions(w->d.n_agents, w->d.batch, actions, flag_out,
                               static_cast<cudaStream_t>(stream));
+}
+
+int ss_check_action_sets(const float* const* bases, int32_t n_sets, int32_t n_agents, int64_t agent_stride,
+                         int64_t n_floats, int32_t* flags, void* stream) {
+  if (!bases || !flags || n_sets < 1 || n_sets > SS_MAX_ROLLOUT || n_agents < 1 ||
+      (int64_t)n_sets * n_agents > 65535 || n_floats < 0 || agent_stride < n_floats) {
+    set_error("check_action_sets: 1.." + std::to_string(SS_MAX_ROLLOUT) + " sets of agent blocks");
+    return SS_ERR_CONTRACT;
+  }
+  for (int s = 0; s < n_sets; ++s)
+    if (!bases[s]) { set_error("check_action_sets: null set"); return SS_ERR_CONTRACT; }
+  if (n_floats == 0) return cuda_status(cudaMemsetAsync(flags, 0, sizeof(int32_t) * n_sets,
+                                                        static_cast<cudaStream_t>(stream)), "flags reset");
+  return launch_check_sets(bases, n_sets, n_agents, agent_stride, n_floats, flags,
+                           static_cast<cudaStream_t>(stream));
 }
 
 int ss_publish_flag(const int32_t* flag, int32_t* host_out, int32_t n, void* stream) {

@@ -219,6 +219,77 @@ int launch_check_actions(int n_agents, int64_t B, const float* const* actions, i
   return cuda_status(cudaGetLastError(), "action check launch");
 }
 
+// NaN scans of up to SS_MAX_ROLLOUT action sets (the steps of a replay) in
+// one launch: blockIdx.y = set * A + agent, a grid-stride pass over that
+// agent's floats along x, the verdict ORed into flags[set].
+struct SetArgs {
+  const float* base[SS_MAX_ROLLOUT];
+  int A;
+  int64_t agent_stride;   // floats between agent blocks of a set
+  int64_t n;              // floats per agent
+  int vec4;
+  int* flags;
+};
+
+__global__ void __launch_bounds__(512) k_check_sets(const SetArgs a) {
+  grid_dep_sync();
+  const int set = blockIdx.y / a.A, agent = blockIdx.y - set * a.A;
+  const float* p = a.base[set] + agent * a.agent_stride;
+  bool bad = false;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a.vec4) {
+    const float4* p4 = reinterpret_cast<const float4*>(p);
+    const int64_t n4 = a.n >> 2;
+    int64_t k = t0;
+    for (; k + 3 * stride < n4; k += 4 * stride) {
+      float4 v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = __ldcs(p4 + k + j * stride);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bad |= isnan(v[j].x) | isnan(v[j].y) | isnan(v[j].z) | isnan(v[j].w);
+    }
+    for (; k < n4; k += stride) {
+      const float4 v = __ldcs(p4 + k);
+      bad |= isnan(v.x) | isnan(v.y) | isnan(v.z) | isnan(v.w);
+    }
+  } else {
+    for (int64_t k = t0; k < a.n; k += stride) bad |= isnan(p[k]);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(a.flags + set, 1);
+}
+
+int launch_check_sets(const float* const* bases, int n_sets, int A, int64_t agent_stride, int64_t n,
+                      int* flags, cudaStream_t st) {
+  SetArgs a;
+  memset(&a, 0, sizeof(a));
+  a.vec4 = (n % 4) == 0 && (agent_stride % 4) == 0;
+  for (int s = 0; s < n_sets; ++s) {
+    a.base[s] = bases[s];
+    a.vec4 &= (reinterpret_cast<uintptr_t>(bases[s]) & 15u) == 0;
+  }
+  a.A = A;
+  a.agent_stride = agent_stride;
+  a.n = n;
+  a.flags = flags;
+  cudaError_t err = cudaMemsetAsync(flags, 0, sizeof(int) * n_sets, st);
+  if (err != cudaSuccess) return cuda_status(err, "action-set flags reset");
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const int64_t per_block = 512LL * (a.vec4 ? 4 : 1);
+  const int64_t want = (n + per_block - 1) / per_block;
+  const int64_t blocks_y = (int64_t)n_sets * A;
+  const int64_t cap = (4LL * sms + blocks_y - 1) / blocks_y;
+  const unsigned gx = (unsigned)std::max<int64_t>(1, std::min(want, cap));
+  launch_step(k_check_sets, dim3(gx, (unsigned)blocks_y), dim3(512), 0, st, a);
+  return cuda_status(cudaGetLastError(), "action-set check launch");
+}
+
 // Copy the verdict words into host-mapped memory with plain stores (PCIe
 // posted writes; no copy engine).
 __global__ void k_publish_flag(const int* flag, int* host_out, int n) {

@@ -393,7 +393,7 @@ class Env:
     def _capture_step(self, ptrs, keepalive, flags=None, n_flags: int = 1) -> StepResult:
         """One fused step without host syncs (graph capture).  flags: device
         int32 NaN verdicts of this and the earlier steps of the replay (their
-        action scans run on a side branch of the graph); any set word makes
+        action scans run ahead of the steps in the graph); any set word makes
         the launch a no-op — the eager validated step's guard, left for the
         host to read after the replay instead of syncing inside it."""
         saved = self.validate
@@ -507,7 +507,7 @@ class StepGraph:
         # kernels of this library per replay: the step kernels (or the one
         # rollout kernel) plus the action scans
         self.launches_per_replay = ((1 + (1 if validate else 0)) if self._fused_rollout
-                                    else S + (S if validate else 0))
+                                    else S + (-(-S // N.MAX_ROLLOUT) if validate else 0))
         self._rng_mode = bool(getattr(sc, "advances_rng_per_step", False))
         world.ensure_device_rng()
         if not env.fused:
@@ -561,19 +561,16 @@ class StepGraph:
                         self._graphs[(cur, i)] = g
                         self._results[(cur, i)] = results
                         continue
-                    scanned = self._capture_scans(env, acts, i, A, B, S, stream) if self.nan_flag is not None else None
+                    if self.nan_flag is not None:
+                        self._capture_scans(acts, i, A, B, S, stream)
                     for k in range(S):
                         act = acts[(i + k) % len(acts)]
                         if self._generic:
                             results.append(self._capture_generic(act))
                             continue
                         base, stride = act.data_ptr(), B * 8
-                        if scanned is not None:
-                            stream.wait_event(scanned[k])
                         results.append(env._capture_step([base + a * stride for a in range(A)], act,
                                                          self.nan_flag, k + 1))
-                    if scanned is not None:
-                        stream.wait_stream(self._side)
                 self._graphs[(cur, i)] = g
                 self._results[(cur, i)] = results
 
@@ -597,28 +594,17 @@ class StepGraph:
                                   infos=[{} for _ in env.agents]))
         return res
 
-    def _capture_scans(self, env, acts, i, A, B, S, stream) -> list:
-        """The replay's S action NaN scans (ss_check_actions) on a side branch
-        of the graph: they depend only on the action buffers, so they run
-        alongside the steps; step k waits for scan k (one event each)."""
-        if not hasattr(self, "_side"):
-            self._side = torch.cuda.Stream(env.device)
-        side = self._side
-        side.wait_stream(stream)           # fork from the capturing stream
-        h = env.scenario.native_handle(env.world)
-        events = []
-        with torch.cuda.stream(side):
-            self.nan_flag.zero_()
-            for k in range(S):
-                act = acts[(i + k) % len(acts)]
-                base, stride = act.data_ptr(), B * 8
-                arr = (N.c_vp * A)(*[base + a * stride for a in range(A)])
-                N.check(N.lib().ss_check_actions(h.handle, arr, self.nan_flag[k:].data_ptr(),
-                                                 side.cuda_stream))
-                ev = torch.cuda.Event()
-                ev.record(side)
-                events.append(ev)
-        return events
+    def _capture_scans(self, acts, i, A, B, S, stream) -> None:
+        """The replay's S action NaN scans as one launch per 16 steps
+        (ss_check_action_sets) on the capturing stream, ahead of the steps:
+        step k then runs only while words 0..k are zero (its guard count),
+        and the step kernels keep their programmatic-launch chain (a scan
+        per step on a side branch put a cross-stream wait before each)."""
+        for k0 in range(0, S, N.MAX_ROLLOUT):
+            n = min(N.MAX_ROLLOUT, S - k0)
+            bases = (N.c_vp * n)(*[acts[(i + k) % len(acts)].data_ptr() for k in range(k0, k0 + n)])
+            N.check(N.lib().ss_check_action_sets(bases, n, A, B * 2, B * 2, self.nan_flag[k0:].data_ptr(),
+                                                 stream.cuda_stream))
 
     def _capture_generic(self, act) -> StepResult:
         env = self.env
