@@ -552,9 +552,12 @@ def run_b200(args, rank, world, local) -> None:
     # ---- end to end through the public API with host buffers --------------
     env_e2e = Env(create_scenario(scen, **ov), B, seed=0, device=dev, validate=True,
                   env_offset=off, global_batch=Bg)
-    E2E_K = max(3, min(K, 10))
     host_acts = [[torch.from_numpy(np.random.default_rng(7 + k).uniform(-1, 1, (B, 2)).astype(np.float32)).pin_memory()
                   for _ in range(A)] for k in range(4)]
+    # enough steps for ~0.3 s of end-to-end stepping (10..300): a 10-step
+    # loop of a small workload lasts a few ms, within reach of one host hiccup
+    calib = max_over_ranks(e2e_rate(env_e2e, host_acts, 3, A, B, O, dev, False), world, dev) / 3
+    E2E_K = int(max_over_ranks(float(min(300, max(10, int(0.3 / max(calib, 1e-6))))), world, dev))
     barrier(world, dev)
     e2e_sec = max_over_ranks(e2e_rate(env_e2e, host_acts, E2E_K, A, B, O, dev, False), world, dev)
     barrier(world, dev)
@@ -615,7 +618,7 @@ def run_b200(args, rank, world, local) -> None:
                                           "timed value loop (same clocks / power state)",
                          "kernel_share_of_step": ms_launch / ms_step, "peak_source": pk["source"]},
             "e2e": {"value": e2e_value, "unit": "agent-steps/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h,
+                    "d2h_bytes_per_step": d2h, "steps": E2E_K,
                     # the host link: the step's D2H (obs dominate) overlaps the
                     # next step's H2D; fraction of the measured pinned D2H copy rate
                     "link_gbs": (h2d + d2h) * E2E_K / e2e_sec / 1e9,
