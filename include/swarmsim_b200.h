@@ -265,9 +265,10 @@ int ss_world_destroy(void* world);
  * dynamics.py:123-184). */
 int ss_env_step(void* world, const SsBuffers* buf, const SsStepIO* io, void* stream);
 
-/* n_steps fused steps in one launch (SsRolloutIO): simple_spread and
- * transport / reverse_transport without sub-steps; SS_ERR_UNSUPPORTED
- * otherwise. */
+/* n_steps fused steps in one launch (SsRolloutIO): simple_spread,
+ * transport / reverse_transport and flocking (1..8 agents) without
+ * sub-steps or joints; SS_ERR_UNSUPPORTED otherwise, SS_ERR_CONTRACT for a
+ * bad step count or a null pointer (nothing launched). */
 int ss_env_rollout(void* world, const SsBuffers* buf, const SsRolloutIO* io, void* stream);
 
 /* Env.reset (env.py:189-198) -> Scenario.reset_world_at.  mask == NULL

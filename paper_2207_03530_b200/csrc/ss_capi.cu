@@ -215,6 +215,11 @@ int ss_env_rollout(void* world, const SsBuffers* buf, const SsRolloutIO* io, voi
     return SS_ERR_CONTRACT;
   }
   if (io->check_actions && !io->guard) { set_error("rollout: check_actions needs guard words"); return SS_ERR_CONTRACT; }
+  for (int s = 0; s < io->n_steps; ++s) {
+    bool ok = io->obs[s] && io->rew[s] && io->done[s];
+    for (int i = 0; i < w->d.n_agents; ++i) ok = ok && io->actions[s * w->d.n_agents + i];
+    if (!ok) { set_error("rollout: null action or output pointer in step " + std::to_string(s)); return SS_ERR_CONTRACT; }
+  }
   return launch_rollout(*w, buf, io, static_cast<cudaStream_t>(stream));
 }
 

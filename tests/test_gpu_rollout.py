@@ -144,3 +144,50 @@ def test_rollout_ragged_batches(cuda, name, B):
             for x, y in zip(outs(ra), outs(rs[s])):
                 assert torch.equal(x, y), f"{name} B={B} S={S_} step {s}"
         np.testing.assert_array_equal(state(a), state(b))
+
+
+def test_rollout_c_abi_contract(cuda):
+    """ss_env_rollout refuses bad step counts, missing pointers, check_actions
+    without guard words (ContractViolation) and worlds without a rollout
+    kernel (SS_ERR_UNSUPPORTED), before launching anything."""
+    import ctypes
+
+    from paper_2207_03530_b200 import _native as N
+
+    B = 64
+    e = S.Env(S.create_scenario("simple_spread"), B, seed=0, device=cuda, validate=False)
+    A = len(e.agents)
+    sc, world = e.scenario, e.world
+    h = sc.native_handle(world)
+    act = torch.zeros((A, B, 2), device=cuda)
+    obs, rew, done = sc.alloc_outputs(world, h.obs_dim)
+
+    def call(n, null_obs=False, check=False, guard=None, handle=h.handle):
+        io = N.SsRolloutIO()
+        acts = (N.c_vp * (max(n, 1) * A))(*([act.data_ptr() + a * B * 8 for a in range(A)] * max(n, 1)))
+        o = (N.c_vp * max(n, 1))(*([None if null_obs else obs.data_ptr()] * max(n, 1)))
+        r = (N.c_vp * max(n, 1))(*([rew.data_ptr()] * max(n, 1)))
+        d = (N.c_vp * max(n, 1))(*([done.data_ptr()] * max(n, 1)))
+        io.n_steps, io.actions, io.obs, io.rew, io.done = n, acts, o, r, d
+        io.obs_agent_stride = obs.shape[1] * obs.shape[2]
+        io.guard = guard
+        io.check_actions = int(check)
+        return N.lib().ss_env_rollout(handle, world.buffers_ref(), ctypes.byref(io),
+                                      torch.cuda.current_stream(cuda).cuda_stream)
+
+    before = state(e)
+    assert call(0) == -1 and call(N.MAX_ROLLOUT + 1) == -1
+    assert call(2, null_obs=True) == -1
+    assert call(2, check=True) == -1
+    d = S.Env(S.create_scenario("dispersion"), B, seed=0, device=cuda, validate=False)
+    hd = d.scenario.native_handle(d.world)
+    io = N.SsRolloutIO()
+    io.n_steps = 1
+    arr = (N.c_vp * 1)(obs.data_ptr())
+    io.obs, io.rew, io.done = arr, arr, arr
+    io.actions = (N.c_vp * len(d.agents))(*([act.data_ptr()] * len(d.agents)))
+    assert N.lib().ss_env_rollout(hd.handle, d.world.buffers_ref(), ctypes.byref(io),
+                                  torch.cuda.current_stream(cuda).cuda_stream) == -5   # SS_ERR_UNSUPPORTED
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(state(e), before)
+    assert call(2) == 0   # and a well-formed call runs
