@@ -419,9 +419,10 @@ class Env:
         step scans its actions and is a no-op once any NaN was seen in the
         replay; StepGraph.check() raises ContractViolation afterwards.
         fused_rollout: the S steps of a replay as ONE launch with the state
-        kept on chip between them (bitwise the same results) — None / True:
-        wherever a rollout kernel exists (simple_spread, transport /
-        reverse_transport, flocking), False: never."""
+        kept on chip between them (bitwise the same results) — None: where
+        the scenario prefers it (simple_spread, transport; flocking from
+        262144 envs), True: wherever a rollout kernel exists (also
+        reverse_transport, any flocking batch), False: never."""
         return StepGraph(self, actions, steps_per_replay, validate, fused_rollout)
 
     @property

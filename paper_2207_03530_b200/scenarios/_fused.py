@@ -151,10 +151,13 @@ class FusedScenario(Scenario):
 
     def rollout_preferred(self, world: World) -> bool:
         """Take the rollout kernel by default (StepGraph fused_rollout=None)
-        wherever it exists: simple_spread and transport are bound by the HBM
+        where it pays: simple_spread and transport are bound by the HBM
         traffic the rollout cuts (1M envs: 57.7 -> 36.6 us per step, 80.2 ->
-        53.8); flocking saves the per-step state traffic and launch ramp too
-        (1M: 306 -> 279 us, 100k: 30.1 -> 29.8)."""
+        53.8); flocking once its state no longer stays in L2 between
+        launches (1M: 306 -> 279 us; 100k, L2-resident: 29.4 vs 29.8,
+        neutral, so the per-step graph)."""
+        if self.native_id == N.SCN_FLOCKING and world.batch_size < 262_144:
+            return False
         return self.rollout_capable(world)
 
     def launch_rollout(self, world: World, step_action_ptrs: list, guard=None, stream: int | None = None,

@@ -84,14 +84,14 @@ def test_rollout_nan_stops_mid_replay(cuda):
 
 def test_rollout_off_and_unsupported_fall_back_to_per_step(cuda):
     """fused_rollout=False, S=1, physics sub-steps, or a scenario without a
-    rollout kernel: the per-step graph; None (default) takes it wherever
-    the scenario prefers it (every world with a rollout kernel)."""
+    rollout kernel: the per-step graph; None (default) takes it where the
+    scenario prefers it (flocking only past L2-resident batch sizes)."""
     B = 64
     for name, ov, S_, fused, want in [("simple_spread", {}, 4, False, False), ("simple_spread", {}, 1, True, False),
                                       ("simple_spread", {"substeps": 2}, 4, True, False),
                                       ("dispersion", {}, 4, True, False), ("transport", {}, 4, True, True),
                                       ("transport", {}, 4, None, True), ("simple_spread", {}, 4, None, True),
-                                      ("flocking", {}, 4, None, True), ("flocking", {}, 4, False, False),
+                                      ("flocking", {}, 4, None, False), ("flocking", {}, 4, True, True),
                                       ("discovery", {}, 4, None, False)]:
         e = S.Env(S.create_scenario(name), B, seed=1, device=cuda, validate=False, **ov)
         A = len(e.agents)
