@@ -212,6 +212,9 @@ SS_DEV float decode_axis(float raw, const SsEntityDesc& d, int raw_forces) {
 #ifndef SS_ROLLOUT_MINB
 #define SS_ROLLOUT_MINB 5   // 5 x 128 threads: <= 96 registers (tools/sweep_variants.py, SWEEP_S=10)
 #endif
+#ifndef SS_ROLLOUT_HALF_CTA
+#define SS_ROLLOUT_HALF_CTA 1
+#endif
 #ifndef SS_ROLLOUT_PREFETCH
 #define SS_ROLLOUT_PREFETCH 1
 #endif

@@ -428,11 +428,17 @@ int launch_transport_rollout(World& w, RolloutArgs& r, cudaStream_t st) {
     if (sms <= 0) sms = 148;
   }
   const bool one_wave6 = grid <= (unsigned)(6 * sms) && grid > (unsigned)(SS_ROLLOUT_MINB * sms);
+  // one-wave case: SS_ROLLOUT_HALF_CTA splits the grid into 64-thread CTAs
+  // (same registers and shared memory per thread), so the SMs get 10-11
+  // CTAs each instead of 5-6 (less tail imbalance inside the single wave)
+  const unsigned bt = (one_wave6 && SS_ROLLOUT_HALF_CTA) ? kSmallThreads / 2 : kSmallThreads;
+  const unsigned g1 = (unsigned)((w.d.batch + bt - 1) / bt);
+  const size_t sh1 = shmem * bt / kSmallThreads;
 #define SS_CASE(n)                                                                                   \
   case n:                                                                                            \
     if (one_wave6) {                                                                                       \
-      if (w.d.si[1]) launch_step(k_transport_rollout<n, 1, 6>, dim3(grid), dim3(kSmallThreads), shmem, st, r); \
-      else launch_step(k_transport_rollout<n, 0, 6>, dim3(grid), dim3(kSmallThreads), shmem, st, r);        \
+      if (w.d.si[1]) launch_step(k_transport_rollout<n, 1, 6>, dim3(g1), dim3(bt), sh1, st, r);             \
+      else launch_step(k_transport_rollout<n, 0, 6>, dim3(g1), dim3(bt), sh1, st, r);                       \
     } else if (w.d.si[1]) {                                                                                \
       launch_step(k_transport_rollout<n, 1, SS_ROLLOUT_MINB>, dim3(grid), dim3(kSmallThreads), shmem, st, r); \
     } else {                                                                                               \
