@@ -186,3 +186,31 @@ def test_validated_step_graph(cuda):
     with pytest.raises(S.ContractViolation, match="NaN"):
         graph.check()
     np.testing.assert_array_equal(state(e), state(ref))
+
+
+def test_validated_step_graph_long_replay(cuda):
+    """validate=True with more steps than one scan launch covers (20 > 16:
+    two ss_check_action_sets calls): clean replays equal eager stepping, a
+    NaN in step 18 stops steps 18.. and is reported by check()."""
+    B, S_ = 96, 20
+    ref = S.Env(S.create_scenario("flocking"), B, seed=2, device=cuda)
+    e = S.Env(S.create_scenario("flocking"), B, seed=2, device=cuda, validate=False)
+    A = len(e.agents)
+    g = torch.Generator(device=cuda)
+    g.manual_seed(21)
+    bufs = [torch.rand((A, B, 2), device=cuda, generator=g) * 2 - 1 for _ in range(2 * S_)]
+    graph = e.step_graph(bufs, steps_per_replay=S_, validate=True)
+    assert not graph.fused_rollout and graph.launches_per_replay == S_ + 2
+    outs = graph.rollout(0)
+    graph.check()
+    for k in range(S_):
+        r = ref.step(bufs[k].clone())
+        for x, y in zip(r.obs + r.rewards, outs[k].obs + outs[k].rewards):
+            assert torch.equal(x, y)
+    bufs[S_ + 18][0, 5, 1] = float("nan")
+    for k in range(S_, S_ + 18):
+        ref.step(bufs[k].clone())
+    graph.rollout(S_)
+    with pytest.raises(S.ContractViolation, match="NaN"):
+        graph.check()
+    np.testing.assert_array_equal(state(e), state(ref))
